@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the QFactor multi-start instantiation hot path on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
+
+A step is one complete qf_instantiate_device call -- every row of SURVEY.md
+Sec. 8a: stage inputs, InitCircuitTensor, TwoSidedSweeps with the per-start
+termination state machine until every start has a verdict, result reduction
+-- over one batch of synthetic inputs already resident in HBM, plus (N > 1)
+the end-of-run exchange: NCCL allgather of per-start summaries, the argmin
+kernel, and the broadcast of the winner's gates.  Weak scaling: every rank
+runs the config's full start count on its own global start range.
+
+metric = converged instantiations/s: starts driven to a terminal verdict per
+second, whole job.  e2e = the same through qf_instantiate with pinned HOST
+buffers (host<->device copies inside the timed region).  roofline = the
+dominant kernel (k_sandwich), algorithmic bytes / CUDA-event time, against
+MEASURED_PEAKS.json.  cpu_baseline / --impl reference = the plain C oracle
+(oracle/) on the host cores, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import qfgen  # noqa: E402
+
+METRIC = "converged instantiations/sec (multi-start, fp64)"
+UNIT = "instantiations/s"
+
+
+def env_int(k, d):
+    return int(os.environ.get(k, d))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(config):
+    """dram bytes per k_sandwich launch from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "sandwich_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    d = json.load(open(p))
+    e = d.get(config)
+    if not e:
+        return None, None
+    return e.get("dram_bytes_per_launch"), e.get("alg_bytes_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.dev)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def config_dict(w, world):
+    return {
+        "workload": f"{w.name}: {w.desc}",
+        "n_qubits": w.n,
+        "gates": w.p,
+        "gate_arities": sorted({len(l) for l in w.locs}),
+        "starts_per_gpu": w.starts,
+        "global_starts": w.starts * world,
+        "target": "self-target V = C(alpha*)" if w.target == "self" else "Haar",
+        "max_iters": w.max_iters,
+        "hyperparams": "P:532 defaults (dist_tol 1e-10, diff_tol_r 1e-5, long_diff 100/0.1, reset 40, beta 0)",
+        "l2": (f"inputs larger than L2: circuit tensors {w.starts * 16 * 4 ** w.n / 2**20:.0f} MiB per GPU "
+               "vs 126 MB L2, no flush" if w.starts * 16 * 4 ** w.n > 126e6 else
+               "working set fits in L2 (reported as such)"),
+        "parallelism": f"starts sharded over {world} GPU(s), weak scaling",
+    }
+
+
+# ---------------------------------------------------------------- oracle legs
+def oracle_sample(w, starts, threads):
+    """Run the plain C oracle on `starts` starts of the workload to verdict."""
+    import oracle
+
+    c = oracle.Circuit(w.n, w.locs, w.kinds, w.const_mats)
+    V = w.target_unitary()
+    init = w.initial(0, starts)
+    P = oracle.default_params(max_iters=w.max_iters)
+    t0 = time.perf_counter()
+    r = oracle.instantiate(c, V, init, P, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return dt, r
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(w):
+    T = host_threads()
+    S = min(2 * T, 256, w.starts)
+    dt, r = oracle_sample(w, S, T)
+    return {"value": S / dt, "unit": UNIT, "cores": int(r.threads), "kind": "oracle",
+            "sample": f"{w.name} global starts [0, {S}) run to verdict by the plain C oracle "
+                      f"({int(r.threads)} threads, {dt:.1f} s, mean {float(np.mean(r.iters)):.0f} sweeps/start)",
+            "seconds": dt}
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    T = host_threads()
+    S = min(T, w.starts)
+    for _ in range(args.warmup):
+        oracle_sample(w, S, T)
+    times, res = [], None
+    for _ in range(args.steps):
+        dt, res = oracle_sample(w, S, T)
+        times.append(dt)
+    tot = sum(times)
+    value = S * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(w, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(res.threads), "kind": "oracle",
+                         "sample": f"each step: {w.name} starts [0, {S}) run to verdict by the "
+                                   f"plain C oracle on {int(res.threads)} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--max-iters", type=int, default=None,
+                    help="override the config's max_iters (not for reported numbers)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    w = qfgen.workload(args.config)
+    if args.max_iters is not None:
+        w.max_iters = args.max_iters
+    if args.impl == "reference":
+        return run_reference(args, w, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_08152_b200 as qf
+    from paper_2306_08152_b200 import dist as qfdist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    S = w.starts
+    start0 = rank * S
+    c = qf.Circuit.from_workload(w)
+    V = np.ascontiguousarray(w.target_unitary())
+    init = w.initial(start0, S)
+    d_V = torch.from_numpy(V).to(dev)
+    d_init = torch.from_numpy(init).to(dev)
+    ws = torch.empty(qf.qf_workspace_size(c, S, max_iters=w.max_iters), dtype=torch.uint8,
+                     device=dev)
+    gates_out = torch.empty_like(d_init)
+    summ = torch.empty(S * 16, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    shard = qfdist.Shard(rank, world, S)
+
+    def step(profile):
+        r = qf.qf_instantiate_device(c, d_V, d_init, ws, stream, d_gates_out=gates_out,
+                                     d_summary_out=summ, max_iters=w.max_iters, profile=profile)
+        best = qfdist.exchange_best(shard, summ, gates_out, stream) if world > 1 else None
+        return r, best
+
+    for _ in range(args.warmup):
+        step(0)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    results = [step(1) for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = [r.stats for r, _ in results]
+    sw_bytes = sum(s["sandwich_bytes"] for s in st)
+    sw_ms = sum(s["sandwich_ms"] for s in st)
+    sw_n = sum(s["sandwich_launches"] for s in st)
+    alg = sum(s["alg_bytes_total"] for s in st)
+    launches = sum(s["kernel_launches"] for s in st) + (args.steps if world > 1 else 0)
+    start_sweeps = sum(s["start_sweeps"] for s in st)
+    last = results[-1][0]
+    verdicts = {qf.VERDICT_NAMES[k]: int((last.verdict == k).sum()) for k in range(1, 6)}
+    successes = int((last.delta < 1e-8).sum())
+    vec = torch.tensor([ms, sw_bytes, alg, float(start_sweeps), float(successes), sw_ms],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max = float(mx[0])
+        alg_sum, ss_sum, succ_sum = float(sm[2]), float(sm[3]), float(sm[4])
+    else:
+        ms_max, alg_sum, ss_sum, succ_sum = ms, alg, float(start_sweeps), float(successes)
+
+    # ---- e2e: qf_instantiate with pinned host buffers, copies inside
+    e2e = None
+    if not args.no_e2e:
+        h_V = torch.from_numpy(V.view(np.float64).copy()).pin_memory()
+        h_init = torch.from_numpy(init).pin_memory()
+        for _ in range(1):
+            qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        rr = [qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters)
+              for _ in range(args.steps)]
+        t_e2e = time.perf_counter() - t0
+        tv = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+        h2d = rr[-1]["h2d_bytes"]
+        d2h = rr[-1]["d2h_bytes"]
+        e2e = {"value": world * S * args.steps / float(tv[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1000 * float(tv[0]) / args.steps,
+               "api": "qf_instantiate (host buffers, pinned)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = load_peaks()
+    achieved = (sw_bytes / 1e9) / (sw_ms / 1e3) if sw_ms > 0 else None
+    dram_per_launch, alg_per_launch_ref = load_traffic(w.name)
+    line = {
+        "metric": METRIC,
+        "value": world * S * args.steps / (ms_max / 1e3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": config_dict(w, world),
+        "sweep_hbm_gbs": (alg_sum / 1e9) / (ms_max / 1e3),
+        "successes_per_s": succ_sum * args.steps / (ms_max / 1e3),
+        "start_sweeps_per_s": ss_sum / (ms_max / 1e3),
+        "verdicts_last_step_rank0": verdicts,
+        "sweeps_per_start_mean": start_sweeps / (S * args.steps),
+        "roofline": {
+            "kernel": "k_sandwich",
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": dram_per_launch,
+            "alg_bytes_per_launch": sw_bytes / sw_n if sw_n else None,
+            "launches": sw_n,
+            "avg_launch_us": 1e3 * sw_ms / sw_n if sw_n else None,
+            "share_of_step": sw_ms / ms if ms > 0 else None,
+            "peak_source": peak_src,
+        },
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(w)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

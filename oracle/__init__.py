@@ -96,7 +96,7 @@ def _declare(L):
     L.oracle_var_doubles.restype = ctypes.c_int
     L.oracle_instantiate.argtypes = [
         ctypes.POINTER(_Circuit), _D, ctypes.c_int, _D, ctypes.POINTER(Params),
-        ctypes.c_int, ctypes.c_int, _D, _I, _I, _D, _D, _D]
+        ctypes.c_int, ctypes.c_int, ctypes.c_int, _D, _I, _I, _D, _D, _D]
     L.oracle_instantiate.restype = ctypes.c_int
 
 
@@ -241,8 +241,10 @@ class Result:
 
 def instantiate(circ: Circuit, target: np.ndarray, initial: np.ndarray,
                 params: Params | None = None, record_sweeps: int = 0,
-                record_gates: bool = False, nthreads: int = 0) -> Result:
-    """Multi-start Qfactor over the S rows of `initial`."""
+                record_gates: bool | int = False, nthreads: int = 0) -> Result:
+    """Multi-start Qfactor over the S rows of `initial`.
+    record_sweeps: costs kept for sweeps 1..R; record_gates: True (gates for
+    the same R sweeps) or an int R_g (gates for sweeps 1..R_g)."""
     params = params or default_params()
     c, keep = circ._c()
     initial = np.ascontiguousarray(initial, dtype=np.float64)
@@ -254,11 +256,12 @@ def instantiate(circ: Circuit, target: np.ndarray, initial: np.ndarray,
     verdict = np.zeros(S, dtype=np.int32)
     gates = np.zeros((S, var))
     R = int(record_sweeps)
+    Rg = (R if record_gates is True else int(record_gates)) if record_gates else 0
     ch = np.zeros((S, max(R, 1)))
-    gh = np.zeros((S, max(R, 1), var)) if record_gates else None
+    gh = np.zeros((S, max(Rg, 1), var)) if Rg else None
     th = lib().oracle_instantiate(
         ctypes.byref(c), _dp(_cplx(target)), S, _dp(initial), ctypes.byref(params),
-        R, int(nthreads), _dp(delta), _ip(iters), _ip(verdict), _dp(gates), _dp(ch),
+        R, Rg, int(nthreads), _dp(delta), _ip(iters), _ip(verdict), _dp(gates), _dp(ch),
         _dp(gh) if gh is not None else None)
     return Result(delta, iters, verdict, gates, ch[:, :R],
-                  gh[:, :R] if gh is not None else None, th)
+                  gh[:, :Rg] if gh is not None else None, th)

@@ -409,7 +409,8 @@ static double delta_of(int n, const double *ct) {
 }
 
 static void run_one(const oracle_circuit *c, const double *target,
-                    const oracle_params *prm, int record_sweeps, double *gates,
+                    const oracle_params *prm, int record_sweeps,
+                    int record_gate_sweeps, double *gates,
                     double *delta, int *iters, int *verdict, double *cost_hist,
                     double *gates_hist) {
   const int N = 1 << c->n, var = oracle_var_doubles(c);
@@ -424,11 +425,9 @@ static void run_one(const oracle_circuit *c, const double *target,
     oracle_sweep(c, ct, gates, prm->beta, 0);
     it++;
     cost[it] = delta_of(c->n, ct); /* once per sweep (reading R9) */
-    if (it <= record_sweeps) {
-      cost_hist[it - 1] = cost[it];
-      if (gates_hist)
-        memcpy(gates_hist + (size_t)(it - 1) * var, gates, sizeof(double) * var);
-    }
+    if (it <= record_sweeps) cost_hist[it - 1] = cost[it];
+    if (gates_hist && it <= record_gate_sweeps)
+      memcpy(gates_hist + (size_t)(it - 1) * var, gates, sizeof(double) * var);
     v = oracle_terminate(prm, it, cost);
     if (v == ORACLE_RUNNING && prm->reset_iters > 0 && it % prm->reset_iters == 0)
       oracle_init_ct(c, target, gates, ct); /* reset_iter (R10) */
@@ -445,7 +444,7 @@ typedef struct {
   const double *target;
   const double *initial;
   const oracle_params *prm;
-  int S, record_sweeps, var;
+  int S, record_sweeps, record_gate_sweeps, var;
   double *delta;
   int *iters, *verdict;
   double *gates_out, *cost_hist, *gates_hist;
@@ -459,11 +458,12 @@ static void *worker(void *arg) {
     if (s >= P->S) break;
     double *g = P->gates_out + (size_t)s * P->var;
     memcpy(g, P->initial + (size_t)s * P->var, sizeof(double) * P->var);
-    run_one(P->c, P->target, P->prm, P->record_sweeps, g, P->delta + s,
+    run_one(P->c, P->target, P->prm, P->record_sweeps, P->record_gate_sweeps, g,
+            P->delta + s,
             P->iters + s, P->verdict + s,
             P->cost_hist + (size_t)s * P->record_sweeps,
             P->gates_hist
-                ? P->gates_hist + (size_t)s * P->record_sweeps * P->var
+                ? P->gates_hist + (size_t)s * P->record_gate_sweeps * P->var
                 : 0);
   }
   return 0;
@@ -471,9 +471,10 @@ static void *worker(void *arg) {
 
 int oracle_instantiate(const oracle_circuit *c, const double *target, int S,
                        const double *initial, const oracle_params *prm,
-                       int record_sweeps, int nthreads, double *delta,
-                       int *iters, int *verdict, double *gates_out,
-                       double *cost_hist, double *gates_hist) {
+                       int record_sweeps, int record_gate_sweeps, int nthreads,
+                       double *delta, int *iters, int *verdict,
+                       double *gates_out, double *cost_hist,
+                       double *gates_hist) {
   if (nthreads <= 0) nthreads = (int)sysconf(_SC_NPROCESSORS_ONLN);
   if (nthreads > S) nthreads = S;
   if (nthreads < 1) nthreads = 1;
@@ -484,6 +485,7 @@ int oracle_instantiate(const oracle_circuit *c, const double *target, int S,
   P.prm = prm;
   P.S = S;
   P.record_sweeps = record_sweeps;
+  P.record_gate_sweeps = gates_hist ? record_gate_sweeps : 0;
   P.var = oracle_var_doubles(c);
   P.delta = delta;
   P.iters = iters;

@@ -100,12 +100,13 @@ int oracle_var_doubles(const oracle_circuit *c);
  * nthreads threads (<=0: one per online core).  initial: S x var_doubles.
  * Outputs (all S-major): delta[S], iters[S], verdict[S], gates_out[S x var],
  * cost_hist[S x record_sweeps] (NaN past the last sweep), gates_hist
- * [S x record_sweeps x var] (may be NULL).  Returns the thread count used. */
+ * [S x record_gate_sweeps x var] (may be NULL).  Returns the thread count. */
 int oracle_instantiate(const oracle_circuit *c, const double *target, int S,
                        const double *initial, const oracle_params *prm,
-                       int record_sweeps, int nthreads, double *delta,
-                       int *iters, int *verdict, double *gates_out,
-                       double *cost_hist, double *gates_hist);
+                       int record_sweeps, int record_gate_sweeps, int nthreads,
+                       double *delta, int *iters, int *verdict,
+                       double *gates_out, double *cost_hist,
+                       double *gates_hist);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,350 @@
+// qf_api.cpp -- the C ABI of include/qf.h: argument validation, handles,
+// errors, host-buffer staging.  All arithmetic of the path runs in the
+// kernels driven by qf_engine.cu; this file only copies and checks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "qf.h"
+#include "qf_internal.h"
+
+namespace qf {
+
+thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+qf_status cuda_fail(cudaError_t e, const char *what) {
+  set_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  return QF_E_CUDA;
+}
+
+}  // namespace qf
+
+using qf::set_error;
+
+namespace {
+
+qf_status fail(qf_status s, const std::string &msg) {
+  set_error(msg);
+  return s;
+}
+
+// max-abs of M^dagger M - I for a d x d interleaved complex matrix
+double unitarity_error(const double *M, int d) {
+  double worst = 0.0;
+  for (int i = 0; i < d; i++)
+    for (int j = 0; j < d; j++) {
+      double re = (i == j) ? -1.0 : 0.0, im = 0.0;
+      for (int k = 0; k < d; k++) {
+        const double ar = M[2 * (k * d + i)], ai = -M[2 * (k * d + i) + 1];
+        const double br = M[2 * (k * d + j)], bi = M[2 * (k * d + j) + 1];
+        re += ar * br - ai * bi;
+        im += ar * bi + ai * br;
+      }
+      const double e = std::max(std::fabs(re), std::fabs(im));
+      if (!(e <= worst)) worst = e;  // NaN-propagating max
+    }
+  return worst;
+}
+
+qf_status check_params(const qf_circuit_s *c, const qf_params *p) {
+  if (!c) return fail(QF_E_ARG, "circuit is NULL");
+  if (!p) return fail(QF_E_ARG, "params is NULL");
+  if (p->num_starts < 1) return fail(QF_E_ARG, "num_starts must be >= 1");
+  if (p->max_iters < 0) return fail(QF_E_ARG, "max_iters must be >= 0");
+  if (p->min_iters < 0) return fail(QF_E_ARG, "min_iters must be >= 0");
+  if (p->reset_iters < 1) return fail(QF_E_ARG, "reset_iters must be >= 1");
+  if (p->long_diff_count < 0) return fail(QF_E_ARG, "long_diff_count must be >= 0");
+  if (!(p->dist_tol > 0.0)) return fail(QF_E_ARG, "dist_tol must be > 0");
+  if (!(p->diff_tol_a >= 0.0) || !(p->diff_tol_r >= 0.0) || !(p->long_diff_r >= 0.0))
+    return fail(QF_E_ARG, "diff_tol_a, diff_tol_r and long_diff_r must be >= 0");
+  if (!(p->beta >= 0.0 && p->beta <= 1.0)) return fail(QF_E_ARG, "beta must lie in [0, 1]");
+  if (p->engine != QF_ENGINE_AUTO && p->engine != QF_ENGINE_STREAM)
+    return fail(QF_E_ARG, "engine not available in this build (AUTO or STREAM)");
+  if (p->record_sweeps < 0 || p->record_count < 0)
+    return fail(QF_E_ARG, "record_sweeps and record_count must be >= 0");
+  if (p->record_count > 0 && p->record_sweeps > 0) {
+    if (!p->record_starts) return fail(QF_E_ARG, "record_starts is NULL");
+    std::vector<char> seen(p->num_starts, 0);
+    for (int i = 0; i < p->record_count; i++) {
+      const int s = p->record_starts[i];
+      if (s < 0 || s >= p->num_starts) return fail(QF_E_ARG, "record_starts index out of range");
+      if (seen[s]) return fail(QF_E_ARG, "record_starts has a repeated index");
+      seen[s] = 1;
+    }
+  }
+  return QF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *qf_last_error(void) { return qf::g_err.c_str(); }
+
+const char *qf_version(void) { return "qfactor-b200 0.1 (sm_100a, complex fp64)"; }
+
+void qf_params_default(qf_params *p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  // PAPER.md P:532
+  p->dist_tol = 1e-10;
+  p->diff_tol_a = 0.0;
+  p->diff_tol_r = 1e-5;
+  p->long_diff_count = 100;
+  p->long_diff_r = 0.1;
+  p->min_iters = 0;
+  p->max_iters = 100000;
+  p->reset_iters = 40;
+  p->beta = 0.0;
+  p->num_starts = 8;
+  p->engine = QF_ENGINE_AUTO;
+  p->record_sweeps = 0;
+  p->record_count = 0;
+  p->record_starts = nullptr;
+}
+
+qf_status qf_circuit_create(int num_qubits, int num_gates, const int *arity,
+                            const int *locations, const int *kinds,
+                            const double *const *const_mats, qf_circuit_t *out) {
+  qf::g_err.clear();
+  if (!out) return fail(QF_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (num_qubits < 1 || num_qubits > 12) return fail(QF_E_DIM, "num_qubits must lie in [1, 12]");
+  if (num_gates < 0) return fail(QF_E_ARG, "num_gates must be >= 0");
+  if (num_gates > 0 && (!arity || !locations || !kinds))
+    return fail(QF_E_ARG, "arity, locations and kinds must be non-NULL");
+  auto *c = new (std::nothrow) qf_circuit_s();
+  if (!c) return fail(QF_E_OOM, "host allocation failed");
+  c->n = num_qubits;
+  c->p = num_gates;
+  int off = 0, voff = 0, coff = 0;
+  for (int k = 0; k < num_gates; k++) {
+    const int m = arity[k];
+    if (m < 1 || m > 3 || m > num_qubits) {
+      delete c;
+      return fail(QF_E_DIM, "gate " + std::to_string(k) + ": arity must lie in [1, min(3, n)]");
+    }
+    for (int t = 0; t < m; t++) {
+      const int q = locations[off + t];
+      if (q < 0 || q >= num_qubits) {
+        delete c;
+        return fail(QF_E_LOCATION, "gate " + std::to_string(k) + ": qubit out of range");
+      }
+      for (int u = 0; u < t; u++)
+        if (locations[off + u] == q) {
+          delete c;
+          return fail(QF_E_LOCATION, "gate " + std::to_string(k) + ": repeated qubit");
+        }
+      c->loc.push_back(q);
+    }
+    c->arity.push_back(m);
+    c->loc_off.push_back(off);
+    off += m;
+    const int dd = 1 << (2 * m);
+    if (kinds[k] == QF_GATE_VARIABLE) {
+      c->kind.push_back(QF_GATE_VARIABLE);
+      c->var_off.push_back(voff);
+      c->const_off.push_back(-1);
+      voff += 2 * dd;
+    } else if (kinds[k] == QF_GATE_CONSTANT) {
+      if (!const_mats || !const_mats[k]) {
+        delete c;
+        return fail(QF_E_ARG, "gate " + std::to_string(k) + ": CONSTANT gate without a matrix");
+      }
+      const double err = unitarity_error(const_mats[k], 1 << m);
+      if (!(err <= 1e-9)) {
+        delete c;
+        return fail(QF_E_NOT_UNITARY, "gate " + std::to_string(k) + ": CONSTANT matrix not unitary");
+      }
+      c->kind.push_back(QF_GATE_CONSTANT);
+      c->var_off.push_back(-1);
+      c->const_off.push_back(coff);
+      c->const_mats.insert(c->const_mats.end(), const_mats[k], const_mats[k] + 2 * dd);
+      coff += 2 * dd;
+    } else {
+      delete c;
+      return fail(QF_E_ARG, "gate " + std::to_string(k) + ": unknown kind");
+    }
+  }
+  c->var_doubles = voff;
+  *out = c;
+  return QF_OK;
+}
+
+void qf_circuit_destroy(qf_circuit_t c) { delete c; }
+
+int qf_circuit_var_doubles(qf_circuit_t c) { return c ? c->var_doubles : -1; }
+
+int qf_circuit_num_qubits(qf_circuit_t c) { return c ? c->n : -1; }
+
+size_t qf_workspace_size(qf_circuit_t c, const qf_params *p) {
+  if (!c || !p || p->num_starts < 1) return 0;
+  return qf::engine_workspace_size(*c, *p);
+}
+
+qf_status qf_instantiate_device(qf_circuit_t c, const double *d_target, const double *d_initial,
+                                const qf_params *p, void *d_workspace, size_t workspace_bytes,
+                                void *stream, double *d_gates_out, qf_summary *d_summary_out,
+                                qf_result_t *out) {
+  qf::g_err.clear();
+  if (out) *out = nullptr;
+  qf_status s = check_params(c, p);
+  if (s != QF_OK) return s;
+  if (!d_target) return fail(QF_E_ARG, "target is NULL");
+  if (!d_initial && c->var_doubles > 0) return fail(QF_E_ARG, "initial is NULL");
+  qf_result_s *r = nullptr;
+  if (out) {
+    r = new (std::nothrow) qf_result_s();
+    if (!r) return fail(QF_E_OOM, "host allocation failed");
+  }
+  qf::EngineOut eo;
+  eo.d_gates_out = d_gates_out;
+  eo.d_summary_out = d_summary_out;
+  eo.host = r;
+  s = qf::engine_run(*c, d_target, d_initial, *p, d_workspace, workspace_bytes,
+                     static_cast<cudaStream_t>(stream), eo);
+  if (s != QF_OK) {
+    delete r;
+    return s;
+  }
+  if (out) *out = r;
+  return QF_OK;
+}
+
+qf_status qf_instantiate(qf_circuit_t c, const double *target, const double *initial,
+                         const qf_params *p, qf_result_t *out) {
+  qf::g_err.clear();
+  if (!out) return fail(QF_E_ARG, "out is NULL");
+  *out = nullptr;
+  qf_status s = check_params(c, p);
+  if (s != QF_OK) return s;
+  if (!target) return fail(QF_E_ARG, "target is NULL");
+  if (!initial && c->var_doubles > 0)
+    return fail(QF_E_ARG, "initial is NULL (pass seeded gates from the input module)");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev < 1) return fail(QF_E_CUDA, "no CUDA device available");
+  const size_t N = (size_t)1 << c->n;
+  const size_t tbytes = N * N * 16, ibytes = (size_t)p->num_starts * c->var_doubles * 8;
+  const size_t wbytes = qf::engine_workspace_size(*c, *p);
+  cudaStream_t st = nullptr;
+  if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
+    return qf::cuda_fail(e, "cudaStreamCreate");
+  char *buf = nullptr;
+  const size_t total = ((tbytes + 255) & ~size_t(255)) + ((ibytes + 255) & ~size_t(255)) + wbytes;
+  e = cudaMallocAsync(reinterpret_cast<void **>(&buf), total, st);
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(st);
+    return fail(QF_E_OOM, std::string("device allocation failed: ") + cudaGetErrorString(e));
+  }
+  char *d_t = buf, *d_i = buf + ((tbytes + 255) & ~size_t(255));
+  char *d_w = d_i + ((ibytes + 255) & ~size_t(255));
+  auto *r = new (std::nothrow) qf_result_s();
+  if (!r) s = fail(QF_E_OOM, "host allocation failed");
+  if (s == QF_OK && (e = cudaMemcpyAsync(d_t, target, tbytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    s = qf::cuda_fail(e, "copy target");
+  if (s == QF_OK && ibytes &&
+      (e = cudaMemcpyAsync(d_i, initial, ibytes, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    s = qf::cuda_fail(e, "copy initial");
+  if (s == QF_OK) {
+    r->stats.h2d_bytes = (long long)(tbytes + ibytes);
+    qf::EngineOut eo;
+    eo.host = r;
+    eo.host_all_gates = true;
+    s = qf::engine_run(*c, reinterpret_cast<double *>(d_t), reinterpret_cast<double *>(d_i), *p,
+                       d_w, wbytes, st, eo);
+  }
+  cudaFreeAsync(buf, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (s != QF_OK) {
+    delete r;
+    return s;
+  }
+  *out = r;
+  return QF_OK;
+}
+
+qf_status qf_result_get(qf_result_t r, int start, double *delta, int *iters, int *verdict,
+                        double *gates) {
+  qf::g_err.clear();
+  if (!r) return fail(QF_E_ARG, "result is NULL");
+  if (start == -1) start = r->best;
+  if (start < 0 || start >= r->num_starts) return fail(QF_E_ARG, "start out of range");
+  const qf_summary &q = r->summary[start];
+  if (delta) *delta = q.delta;
+  if (iters) *iters = q.iters;
+  if (verdict) *verdict = q.verdict;
+  if (gates && r->var_doubles > 0) {
+    if (r->all_gates) {
+      std::memcpy(gates, r->gates.data() + (size_t)start * r->var_doubles, r->var_doubles * 8);
+    } else if (start == r->best && !r->gates.empty()) {
+      std::memcpy(gates, r->gates.data(), r->var_doubles * 8);
+    } else {
+      return fail(QF_E_ARG, "gates of this start are not held by the result (device call)");
+    }
+  }
+  return QF_OK;
+}
+
+int qf_result_best(qf_result_t r) { return r ? r->best : -1; }
+
+int qf_result_num_starts(qf_result_t r) { return r ? r->num_starts : 0; }
+
+qf_status qf_result_trace(qf_result_t r, int i, double *costs, double *gates_per_sweep, int *len) {
+  qf::g_err.clear();
+  if (!r) return fail(QF_E_ARG, "result is NULL");
+  if (i < 0 || i >= r->record_count) return fail(QF_E_ARG, "record index out of range");
+  const int R = r->record_sweeps;
+  if (costs) std::memcpy(costs, r->rec_cost.data() + (size_t)i * R, (size_t)R * 8);
+  if (gates_per_sweep && r->var_doubles > 0)
+    std::memcpy(gates_per_sweep, r->rec_gates.data() + (size_t)i * R * r->var_doubles,
+                (size_t)R * r->var_doubles * 8);
+  if (len) {
+    int n = 0;
+    while (n < R && !std::isnan(r->rec_cost[(size_t)i * R + n])) n++;
+    *len = n;
+  }
+  return QF_OK;
+}
+
+qf_status qf_result_stats(qf_result_t r, qf_stats *stats) {
+  if (!r || !stats) return fail(QF_E_ARG, "NULL argument");
+  *stats = r->stats;
+  return QF_OK;
+}
+
+void qf_result_destroy(qf_result_t r) { delete r; }
+
+qf_status qf_select_best_device(const qf_summary *d_summaries, int64_t count, void *stream,
+                                int64_t *d_best_index) {
+  qf::g_err.clear();
+  if (!d_summaries || !d_best_index || count < 1) return fail(QF_E_ARG, "bad argument");
+  return qf::select_best_device(d_summaries, count, static_cast<cudaStream_t>(stream),
+                                reinterpret_cast<long long *>(d_best_index));
+}
+
+qf_status qf_select_best_host(const qf_summary *s, int64_t count, int64_t *best_index) {
+  qf::g_err.clear();
+  if (!s || !best_index || count < 1) return fail(QF_E_ARG, "bad argument");
+  int64_t best = -1;
+  for (int64_t i = 0; i < count; i++) {
+    const double d = s[i].delta;
+    if (std::isnan(d)) {
+      if (best < 0) best = i;
+      continue;
+    }
+    if (best < 0 || std::isnan(s[best].delta) || d < s[best].delta) best = i;
+  }
+  *best_index = best;
+  return QF_OK;
+}
+
+}  // extern "C"

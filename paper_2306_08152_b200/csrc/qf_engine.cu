@@ -1,0 +1,725 @@
+// qf_engine.cu -- per-device engine of the QFactor multi-start sweep (host C++
+// driving the sm_100a kernels of qf_kernels.cuh).
+//
+// One call = the whole hot path of SURVEY.md Sec. 8a for S starts:
+//   a1 stage inputs      V^dagger, packed gates copy, unitarity checks
+//   a2 init / reset      ct_s <- E(u_p)...E(u_1) V^dagger
+//   a3-a6 TwoSidedSweep  per gate step: k_env_polar (env + polar update) then
+//                        k_sandwich (fused peel + re-apply)
+//   a7 cost + mask       k_trace_mask + k_compact after every sweep
+//   a8 result reduction  summaries + argmin kernel
+// Finished starts leave the active list, so they stop costing bandwidth.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "qf_internal.h"
+#include "qf_kernels.cuh"
+
+namespace qf {
+
+namespace {
+
+constexpr int kRingMin = 2;
+
+// CUDA-event timing of individual launches (qf_params.profile = 1): a ring of
+// event pairs, harvested when a slot is reused and at the end of the call.
+struct Profiler {
+  static constexpr int kRing = 512;
+  bool on = false;
+  cudaEvent_t beg[kRing] = {}, end[kRing] = {};
+  int kind[kRing] = {};
+  int next = 0, used = 0;
+  double ms[2] = {0.0, 0.0};
+  void init() {
+    for (int i = 0; i < kRing; i++) {
+      cudaEventCreate(&beg[i]);
+      cudaEventCreate(&end[i]);
+      kind[i] = -1;
+    }
+    on = true;
+  }
+  ~Profiler() {
+    if (!on) return;
+    for (int i = 0; i < kRing; i++) {
+      cudaEventDestroy(beg[i]);
+      cudaEventDestroy(end[i]);
+    }
+  }
+  void harvest(int i) {
+    if (!on || kind[i] < 0) return;
+    float t = 0.f;
+    cudaEventSynchronize(end[i]);
+    cudaEventElapsedTime(&t, beg[i], end[i]);
+    ms[kind[i]] += t;
+    kind[i] = -1;
+  }
+  int open(int k, cudaStream_t st) {
+    const int i = next;
+    next = (next + 1) % kRing;
+    harvest(i);
+    kind[i] = k;
+    cudaEventRecord(beg[i], st);
+    return i;
+  }
+  void close(int i, cudaStream_t st) { cudaEventRecord(end[i], st); }
+  void drain() {
+    if (!on) return;
+    for (int i = 0; i < kRing; i++) harvest(i);
+  }
+};
+
+// ------------------------------------------------------------------ aux kernels
+__global__ void k_vdag(const double2 *V, double2 *Vd, int N) {
+  const long long NN = (long long)N * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < NN;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    const double2 v = V[(long long)j * N + i];
+    Vd[e] = make_double2(v.x, -v.y);
+  }
+}
+
+// max-abs of V^dagger V - I over one (i, j) per thread; flags > tol (or NaN)
+__global__ void k_check_target(const double2 *V, int N, double tol, int *bad) {
+  const long long NN = (long long)N * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < NN;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    double2 acc = make_double2(i == j ? -1.0 : 0.0, 0.0);
+    for (int k = 0; k < N; k++) acc = cfma_cj(V[(long long)k * N + i], V[(long long)k * N + j], acc);
+    if (!(fabs(acc.x) <= tol && fabs(acc.y) <= tol)) atomicOr(bad, 1);
+  }
+}
+
+// unitarity of every VARIABLE initial gate: one thread per (start, gate)
+__global__ void k_check_gates(const double *G, long long S, int nvar, const int2 *tab,
+                              int var_doubles, double tol, int *bad) {
+  const long long total = S * nvar;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long s = e / nvar;
+    const int2 g = tab[e % nvar];  // (offset in doubles, d)
+    const double2 *u = reinterpret_cast<const double2 *>(G + s * var_doubles + g.x);
+    const int d = g.y;
+    double worst = 0.0;
+    for (int i = 0; i < d; i++)
+      for (int j = 0; j < d; j++) {
+        double2 acc = make_double2(i == j ? -1.0 : 0.0, 0.0);
+        for (int k = 0; k < d; k++) acc = cfma_cj(u[k * d + i], u[k * d + j], acc);
+        worst = fmax(worst, fmax(fabs(acc.x), fabs(acc.y)));
+        if (!(fabs(acc.x) <= tol && fabs(acc.y) <= tol)) worst = INFINITY;
+      }
+    if (!(worst <= tol)) atomicOr(bad, 2);
+  }
+}
+
+__global__ void k_iota(int *active, int *n_active, int S, int *rec_slot) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    active[s] = s;
+    rec_slot[s] = -1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_active = S;
+}
+
+__global__ void k_set_slots(int *rec_slot, const int *starts, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) rec_slot[starts[i]] = i;
+}
+
+// ct_s <- V^dagger for every active start
+__global__ void k_ct_from_vdag(double2 *ct, long long NN, const double2 *Vd, const int *active,
+                               const int *n_active) {
+  const long long total = (long long)(*n_active) * NN;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long ai = e / NN, k = e - ai * NN;
+    ct[(long long)active[ai] * NN + k] = Vd[k];
+  }
+}
+
+__global__ void k_summaries(const double *delta, const int *iters, const int *verdict, int S,
+                            qf_summary *out) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
+    qf_summary q;
+    q.delta = delta[s];
+    q.iters = iters[s];
+    q.verdict = verdict[s];
+    out[s] = q;
+  }
+}
+
+// best = argmin delta, ties -> lowest index, NaN never wins (total order on
+// (delta, index) => the result does not depend on the reduction order).
+__device__ __forceinline__ bool better(double d1, long long i1, double d2, long long i2) {
+  if (isnan(d2)) return !isnan(d1) || i1 < i2;
+  if (isnan(d1)) return false;
+  return d1 < d2 || (d1 == d2 && i1 < i2);
+}
+
+__global__ void __launch_bounds__(1024) k_select_best(const qf_summary *q, long long count,
+                                                      long long *best) {
+  __shared__ double sd[1024];
+  __shared__ long long si[1024];
+  double bd = NAN;
+  long long bi = -1;
+  for (long long i = threadIdx.x; i < count; i += blockDim.x) {
+    const double d = q[i].delta;
+    if (bi < 0 || better(d, i, bd, bi)) {
+      bd = d;
+      bi = i;
+    }
+  }
+  sd[threadIdx.x] = bd;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      const double d2 = sd[threadIdx.x + off];
+      const long long i2 = si[threadIdx.x + off];
+      if (i2 >= 0 && (si[threadIdx.x] < 0 || better(d2, i2, sd[threadIdx.x], si[threadIdx.x]))) {
+        sd[threadIdx.x] = d2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *best = si[0];
+}
+
+// ------------------------------------------------------------------ host helpers
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
+      rec_slot, rec_starts, rec_cost, rec_gates, summary, best, total;
+  int ring;
+};
+
+Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
+  Layout L{};
+  const size_t S = (size_t)p.num_starts, N = (size_t)1 << c.n;
+  const size_t R = (size_t)std::max(0, p.record_sweeps), rc = (size_t)std::max(0, p.record_count);
+  L.ring = std::max(kRingMin, p.long_diff_count + 1);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes);
+    return at;
+  };
+  L.ct = take(S * N * N * 16);
+  L.gates = take(S * (size_t)c.var_doubles * 8);
+  L.scratch = take(S * kScratch * 16);
+  L.vdag = take(N * N * 16);
+  L.cmats = take(std::max<size_t>(1, c.const_mats.size()) * 8);
+  L.gtab = take((size_t)std::max(1, c.p) * 8);
+  L.hist = take(S * (size_t)L.ring * 8);
+  L.delta = take(S * 8);
+  L.iters = take(S * 4);
+  L.verdict = take(S * 4);
+  L.active = take(S * 4);
+  L.counters = take(64);
+  L.rec_slot = take(S * 4);
+  L.rec_starts = take(std::max<size_t>(1, rc) * 4);
+  L.rec_cost = take(std::max<size_t>(1, rc * R) * 8);
+  L.rec_gates = take(std::max<size_t>(1, rc * R * (size_t)c.var_doubles) * 8);
+  L.summary = take(S * sizeof(qf_summary));
+  L.best = take(16);
+  L.total = o;
+  return L;
+}
+
+int ilog2(int x) {
+  int k = 0;
+  while ((1 << k) < x) k++;
+  return k;
+}
+
+Bits make_bits(const qf_circuit_s &c, int k) {
+  Bits b{};
+  b.n = c.n;
+  b.m = c.arity[k];
+  b.d = 1 << b.m;
+  const int *loc = &c.loc[c.loc_off[k]];
+  for (int a = 0; a < b.d; a++) {
+    int x = 0;
+    for (int t = 0; t < b.m; t++) x |= ((a >> (b.m - 1 - t)) & 1) << (c.n - 1 - loc[t]);
+    b.abits[a] = x;
+  }
+  int r = 0;
+  for (int pos = 0; pos < c.n; pos++) {
+    bool in = false;
+    for (int t = 0; t < b.m; t++) in |= (c.n - 1 - loc[t]) == pos;
+    if (!in) b.rest_pos[r++] = pos;
+  }
+  return b;
+}
+
+// tile geometry of k_sandwich for gate k (see SandwichArgs)
+void make_tiles(const qf_circuit_s &c, int k, SandwichArgs &A) {
+  A.b = make_bits(c, k);
+  const int N = 1 << c.n, d = A.b.d, m = A.b.m;
+  A.N = N;
+  A.DC = std::min(N, kTileItems);
+  A.CT = A.DC / d;
+  A.RT = std::min(N / d, kTileItems / A.DC);
+  A.TC = (N / d) / A.CT;
+  A.tiles_per_start = ((N / d) / A.RT) * A.TC;
+  A.log_ct = ilog2(A.CT);
+  A.log_dc = ilog2(A.DC);
+  std::vector<int> free_bits;
+  const int *loc = &c.loc[c.loc_off[k]];
+  for (int t = 0; t < m; t++) free_bits.push_back(c.n - 1 - loc[t]);
+  for (int q = 0; q < A.log_ct; q++) free_bits.push_back(A.b.rest_pos[q]);
+  std::sort(free_bits.begin(), free_bits.end());
+  for (int q = 0; q < A.log_dc; q++) A.col_dep[q] = free_bits[q];
+  auto index_of = [&](int pos) {
+    return (int)(std::find(free_bits.begin(), free_bits.end(), pos) - free_bits.begin());
+  };
+  for (int b = 0; b < d; b++) {
+    int x = 0;
+    for (int t = 0; t < m; t++)
+      x |= ((b >> (m - 1 - t)) & 1) << index_of(c.n - 1 - loc[t]);
+    A.jt_b[b] = x;
+  }
+  for (int q = 0; q < A.log_ct; q++) A.jt_rest[q] = index_of(A.b.rest_pos[q]);
+}
+
+struct Engine {
+  const qf_circuit_s &c;
+  const qf_params &p;
+  cudaStream_t st;
+  char *ws;
+  Layout L;
+  int S, N, nsm = 148;
+  long long launches = 0;
+  int sandwich_grid[4] = {0, 0, 0, 0};
+  // byte accounting: launches per "context" j; the active count in context j
+  // is n_active after sweep j (context 0 = the initial S)
+  int ctx = 0;
+  std::vector<long long> sw_ctx, env_ctx, env_bytes_ctx;
+  Profiler prof;
+
+  double2 *ct() const { return reinterpret_cast<double2 *>(ws + L.ct); }
+  double *gates() const { return reinterpret_cast<double *>(ws + L.gates); }
+  double2 *scratch() const { return reinterpret_cast<double2 *>(ws + L.scratch); }
+  double2 *vdag() const { return reinterpret_cast<double2 *>(ws + L.vdag); }
+  double2 *cmats() const { return reinterpret_cast<double2 *>(ws + L.cmats); }
+  int *active() const { return reinterpret_cast<int *>(ws + L.active); }
+  int *n_active() const { return reinterpret_cast<int *>(ws + L.counters); }
+  int *bad() const { return reinterpret_cast<int *>(ws + L.counters) + 1; }
+
+  Engine(const qf_circuit_s &c_, const qf_params &p_, cudaStream_t st_, void *ws_)
+      : c(c_), p(p_), st(st_), ws(static_cast<char *>(ws_)), L(make_layout(c_, p_)) {
+    S = p.num_starts;
+    N = 1 << c.n;
+    sw_ctx.assign((size_t)p.max_iters + 2, 0);
+    env_ctx.assign((size_t)p.max_iters + 2, 0);
+    env_bytes_ctx.assign((size_t)p.max_iters + 2, 0);
+    if (p.profile) prof.init();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+
+  template <int D>
+  cudaError_t launch_sandwich(const SandwichArgs &A) {
+    const size_t smem = (size_t)(D * kTileItems + 2 * D * D) * sizeof(double2);
+    int &grid = sandwich_grid[ilog2(D)];
+    if (grid == 0) {
+      cudaFuncSetAttribute(k_sandwich<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sandwich<D>, kTileItems, smem);
+      grid = std::max(1, per_sm) * nsm;
+    }
+    const long long total = (long long)S * A.tiles_per_start;
+    const int g = (int)std::max<long long>(1, std::min<long long>(grid, total));
+    const int slot = prof.on ? prof.open(0, st) : -1;
+    k_sandwich<D><<<g, kTileItems, smem, st>>>(A);
+    if (slot >= 0) prof.close(slot, st);
+    launches++;
+    sw_ctx[ctx]++;
+    return cudaGetLastError();
+  }
+
+  cudaError_t sandwich(const SandwichArgs &A) {
+    switch (A.b.d) {
+      case 2: return launch_sandwich<2>(A);
+      case 4: return launch_sandwich<4>(A);
+      default: return launch_sandwich<8>(A);
+    }
+  }
+
+  template <int D>
+  cudaError_t launch_env(const EnvArgs &A) {
+    const int g = std::max(1, std::min((S + kEnvWarps - 1) / kEnvWarps, nsm * 16));
+    const int slot = prof.on ? prof.open(1, st) : -1;
+    k_env_polar<D><<<g, 32 * kEnvWarps, 0, st>>>(A);
+    if (slot >= 0) prof.close(slot, st);
+    launches++;
+    env_ctx[ctx]++;
+    env_bytes_ctx[ctx] += (long long)16 * N * D + 64LL * D * D;  // gather + gate r/w
+    return cudaGetLastError();
+  }
+
+  cudaError_t env(int k, int forward) {
+    EnvArgs A{};
+    A.b = make_bits(c, k);
+    A.N = N;
+    A.ct = ct();
+    A.ct_stride = (long long)N * N;
+    A.active = active();
+    A.n_active = n_active();
+    A.gates = reinterpret_cast<double2 *>(gates());
+    A.gstride = c.var_doubles / 2;
+    A.goff = c.var_off[k] / 2;
+    A.scratch = scratch();
+    A.forward = forward;
+    A.beta = p.beta;
+    switch (A.b.d) {
+      case 2: return launch_env<2>(A);
+      case 4: return launch_env<4>(A);
+      default: return launch_env<8>(A);
+    }
+  }
+
+  // operand descriptors: the per-start VARIABLE gate, the u_old scratch, or a
+  // CONSTANT matrix shared by all starts (stride 0)
+  void gate_operand(int k, const double2 *&src, long long &stride) const {
+    if (c.kind[k] == QF_GATE_VARIABLE) {
+      src = reinterpret_cast<const double2 *>(gates()) + c.var_off[k] / 2;
+      stride = c.var_doubles / 2;
+    } else {
+      src = cmats() + c.const_off[k] / 2;
+      stride = 0;
+    }
+  }
+  void old_operand(int k, const double2 *&src, long long &stride) const {
+    if (c.kind[k] == QF_GATE_VARIABLE) {
+      src = scratch();
+      stride = kScratch;
+    } else {
+      gate_operand(k, src, stride);
+    }
+  }
+
+  SandwichArgs base_args(int k) const {
+    SandwichArgs A{};
+    make_tiles(c, k, A);
+    A.ct = ct();
+    A.ct_stride = (long long)N * N;
+    A.active = active();
+    A.n_active = n_active();
+    return A;
+  }
+
+  // one gate step of TwoSidedSweep (P:599-605 backward, P:610-616 forward)
+  cudaError_t step(int k, int forward) {
+    cudaError_t e = cudaSuccess;
+    if (c.kind[k] == QF_GATE_VARIABLE && (e = env(k, forward)) != cudaSuccess) return e;
+    SandwichArgs A = base_args(k);
+    if (!forward) {  // ct <- E(u_old)^dagger ct E(u_new)
+      old_operand(k, A.lsrc, A.lstride);
+      A.ldag = 1;
+      gate_operand(k, A.rsrc, A.rstride);
+      A.rdag = 0;
+    } else {         // ct <- E(u_new) ct E(u_old)^dagger
+      gate_operand(k, A.lsrc, A.lstride);
+      A.ldag = 0;
+      old_operand(k, A.rsrc, A.rstride);
+      A.rdag = 1;
+    }
+    return sandwich(A);
+  }
+
+  // InitCircuitTensor for the active starts
+  cudaError_t init_ct() {
+    const long long NN = (long long)N * N;
+    const int g = (int)std::max<long long>(1, std::min<long long>((S * NN + 255) / 256, nsm * 32));
+    k_ct_from_vdag<<<g, 256, 0, st>>>(ct(), NN, vdag(), active(), n_active());
+    launches++;
+    cudaError_t e = cudaGetLastError();
+    for (int k = 0; k < c.p && e == cudaSuccess; k++) {
+      SandwichArgs A = base_args(k);
+      gate_operand(k, A.lsrc, A.lstride);
+      A.ldag = 0;
+      A.rsrc = nullptr;
+      e = sandwich(A);
+    }
+    return e;
+  }
+
+  cudaError_t trace(int it) {
+    TraceArgs A{};
+    A.N = N;
+    A.ct = ct();
+    A.ct_stride = (long long)N * N;
+    A.active = active();
+    A.n_active = n_active();
+    A.it = it;
+    A.dist_tol = p.dist_tol;
+    A.diff_tol_a = p.diff_tol_a;
+    A.diff_tol_r = p.diff_tol_r;
+    A.long_diff_r = p.long_diff_r;
+    A.long_diff_count = p.long_diff_count;
+    A.min_iters = p.min_iters;
+    A.max_iters = p.max_iters;
+    A.ring = L.ring;
+    A.hist = reinterpret_cast<double *>(ws + L.hist);
+    A.delta = reinterpret_cast<double *>(ws + L.delta);
+    A.iters = reinterpret_cast<int *>(ws + L.iters);
+    A.verdict = reinterpret_cast<int *>(ws + L.verdict);
+    A.rec_slot = reinterpret_cast<int *>(ws + L.rec_slot);
+    A.R = (p.record_count > 0) ? p.record_sweeps : 0;
+    A.rec_cost = reinterpret_cast<double *>(ws + L.rec_cost);
+    A.rec_gates = reinterpret_cast<double *>(ws + L.rec_gates);
+    A.gates = gates();
+    A.var_doubles = c.var_doubles;
+    const int g = std::max(1, std::min((S + kTraceWarps - 1) / kTraceWarps, nsm * 8));
+    k_trace_mask<<<g, 32 * kTraceWarps, 0, st>>>(A);
+    launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || it == 0) return e;
+    k_compact<<<1, 1024, 0, st>>>(active(), n_active(), reinterpret_cast<int *>(ws + L.verdict));
+    launches++;
+    return cudaGetLastError();
+  }
+};
+
+}  // namespace
+
+size_t engine_workspace_size(const qf_circuit_s &c, const qf_params &p) {
+  return make_layout(c, p).total;
+}
+
+#define QF_CHECK(expr)                                   \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr);  \
+  } while (0)
+
+qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double *d_initial,
+                     const qf_params &p, void *ws, size_t ws_bytes, cudaStream_t st,
+                     const EngineOut &out) {
+  Engine E(c, p, st, ws);
+  if (ws == nullptr || ws_bytes < E.L.total) {
+    set_error("workspace too small: need " + std::to_string(E.L.total) + " bytes");
+    return QF_E_OOM;
+  }
+  const int S = p.num_starts, N = 1 << c.n;
+  char *W = static_cast<char *>(ws);
+  long long h2d = 0, d2h = 0;
+
+  // ---- a1: stage inputs
+  if (!c.const_mats.empty()) {
+    QF_CHECK(cudaMemcpyAsync(W + E.L.cmats, c.const_mats.data(), c.const_mats.size() * 8,
+                             cudaMemcpyHostToDevice, st));
+    h2d += (long long)c.const_mats.size() * 8;
+  }
+  std::vector<int2> tab;
+  for (int k = 0; k < c.p; k++)
+    if (c.kind[k] == QF_GATE_VARIABLE) tab.push_back(make_int2(c.var_off[k], 1 << c.arity[k]));
+  if (!tab.empty()) {
+    QF_CHECK(cudaMemcpyAsync(W + E.L.gtab, tab.data(), tab.size() * sizeof(int2),
+                             cudaMemcpyHostToDevice, st));
+    h2d += (long long)(tab.size() * sizeof(int2));
+  }
+  QF_CHECK(cudaMemsetAsync(E.bad(), 0, sizeof(int), st));
+  const int g1 = std::max(1, std::min((int)(((long long)N * N + 255) / 256), E.nsm * 8));
+  k_vdag<<<g1, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), E.vdag(), N);
+  k_check_target<<<g1, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), N, 1e-9, E.bad());
+  E.launches += 2;
+  if (!tab.empty()) {
+    const long long tot = (long long)S * tab.size();
+    const int g2 = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, E.nsm * 16));
+    k_check_gates<<<g2, 256, 0, st>>>(d_initial, S, (int)tab.size(),
+                                      reinterpret_cast<const int2 *>(W + E.L.gtab), c.var_doubles,
+                                      1e-9, E.bad());
+    E.launches++;
+  }
+  QF_CHECK(cudaGetLastError());
+  if (c.var_doubles > 0)
+    QF_CHECK(cudaMemcpyAsync(E.gates(), d_initial, (size_t)S * c.var_doubles * 8,
+                             cudaMemcpyDeviceToDevice, st));
+  int *rec_slot = reinterpret_cast<int *>(W + E.L.rec_slot);
+  k_iota<<<std::max(1, std::min((S + 255) / 256, E.nsm * 4)), 256, 0, st>>>(E.active(), E.n_active(),
+                                                                             S, rec_slot);
+  E.launches++;
+  if (p.record_count > 0 && p.record_sweeps > 0) {
+    QF_CHECK(cudaMemcpyAsync(W + E.L.rec_starts, p.record_starts, (size_t)p.record_count * 4,
+                             cudaMemcpyHostToDevice, st));
+    h2d += (long long)p.record_count * 4;
+    const size_t rcn = (size_t)p.record_count * p.record_sweeps;
+    std::vector<double> nans(rcn, NAN);
+    QF_CHECK(cudaMemcpyAsync(W + E.L.rec_cost, nans.data(), rcn * 8, cudaMemcpyHostToDevice, st));
+    h2d += (long long)rcn * 8;
+    QF_CHECK(cudaMemsetAsync(W + E.L.rec_gates, 0, rcn * (size_t)c.var_doubles * 8, st));
+    k_set_slots<<<(p.record_count + 255) / 256, 256, 0, st>>>(
+        rec_slot, reinterpret_cast<const int *>(W + E.L.rec_starts), p.record_count);
+    E.launches++;
+  }
+  QF_CHECK(cudaGetLastError());
+  // pinned host words: [0] input flags, [1 + j] = n_active after sweep j
+  int *h_flags = nullptr;
+  QF_CHECK(cudaHostAlloc(&h_flags, ((size_t)p.max_iters + 3) * sizeof(int), cudaHostAllocDefault));
+  struct Pinned {
+    int *p;
+    ~Pinned() { cudaFreeHost(p); }
+  } pinned{h_flags};
+  int *h_nact = h_flags + 1;
+  h_nact[0] = S;
+  QF_CHECK(cudaMemcpyAsync(h_flags, E.bad(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  QF_CHECK(cudaStreamSynchronize(st));
+  d2h += 4;
+  if (h_flags[0] & 1) {
+    set_error("target is not unitary to 1e-9 (max-abs of V^dagger V - I)");
+    return QF_E_NOT_UNITARY;
+  }
+  if (h_flags[0] & 2) {
+    set_error("an initial VARIABLE gate is not unitary to 1e-9");
+    return QF_E_NOT_UNITARY;
+  }
+
+  // ---- a2: InitCircuitTensor
+  E.ctx = 0;
+  QF_CHECK(E.init_ct());
+
+  // ---- a3..a7: sweeps until every start has a verdict
+  cudaEvent_t ev[2];
+  QF_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  QF_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct Events {
+    cudaEvent_t *e;
+    ~Events() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } events{ev};
+  int last = 0;  // last sweep enqueued
+  if (p.max_iters == 0) {
+    QF_CHECK(E.trace(0));
+  } else {
+    for (int it = 1; it <= p.max_iters; it++) {
+      E.ctx = it - 1;  // this sweep runs on the starts active after sweep it-1
+      for (int k = c.p - 1; k >= 0; k--) QF_CHECK(E.step(k, 0));
+      for (int k = 0; k < c.p; k++) QF_CHECK(E.step(k, 1));
+      QF_CHECK(E.trace(it));
+      E.ctx = it;
+      if (p.reset_iters > 0 && it % p.reset_iters == 0 && it < p.max_iters) QF_CHECK(E.init_ct());
+      QF_CHECK(cudaMemcpyAsync(&h_nact[it], E.n_active(), sizeof(int), cudaMemcpyDeviceToHost, st));
+      QF_CHECK(cudaEventRecord(ev[it & 1], st));
+      d2h += 4;
+      last = it;
+      // lagged check: the GPU keeps one sweep queued while the host waits
+      if (it >= 2) {
+        QF_CHECK(cudaEventSynchronize(ev[(it - 1) & 1]));
+        if (h_nact[it - 1] == 0) break;
+      }
+      if (it == p.max_iters) break;
+    }
+  }
+
+  // ---- a8: summaries and best start
+  qf_summary *summ = out.d_summary_out ? out.d_summary_out
+                                       : reinterpret_cast<qf_summary *>(W + E.L.summary);
+  k_summaries<<<std::max(1, std::min((S + 255) / 256, E.nsm * 4)), 256, 0, st>>>(
+      reinterpret_cast<double *>(W + E.L.delta), reinterpret_cast<int *>(W + E.L.iters),
+      reinterpret_cast<int *>(W + E.L.verdict), S, summ);
+  long long *d_best = reinterpret_cast<long long *>(W + E.L.best);
+  k_select_best<<<1, 1024, 0, st>>>(summ, S, d_best);
+  E.launches += 2;
+  QF_CHECK(cudaGetLastError());
+  if (out.d_gates_out && c.var_doubles > 0)
+    QF_CHECK(cudaMemcpyAsync(out.d_gates_out, E.gates(), (size_t)S * c.var_doubles * 8,
+                             cudaMemcpyDeviceToDevice, st));
+  if (out.host) {
+    qf_result_s &r = *out.host;
+    r.num_starts = S;
+    r.var_doubles = c.var_doubles;
+    r.summary.resize(S);
+    long long best = -1;
+    QF_CHECK(cudaMemcpyAsync(r.summary.data(), summ, (size_t)S * sizeof(qf_summary),
+                             cudaMemcpyDeviceToHost, st));
+    QF_CHECK(cudaMemcpyAsync(&best, d_best, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    QF_CHECK(cudaStreamSynchronize(st));
+    d2h += (long long)S * sizeof(qf_summary) + 8;
+    r.best = (int)best;
+    r.all_gates = out.host_all_gates;
+    if (c.var_doubles > 0) {
+      if (out.host_all_gates) {
+        r.gates.resize((size_t)S * c.var_doubles);
+        QF_CHECK(cudaMemcpyAsync(r.gates.data(), E.gates(), r.gates.size() * 8,
+                                 cudaMemcpyDeviceToHost, st));
+      } else if (best >= 0) {
+        r.gates.resize((size_t)c.var_doubles);
+        QF_CHECK(cudaMemcpyAsync(r.gates.data(), E.gates() + (size_t)best * c.var_doubles,
+                                 r.gates.size() * 8, cudaMemcpyDeviceToHost, st));
+      }
+      d2h += (long long)r.gates.size() * 8;
+    }
+    r.record_sweeps = (p.record_count > 0) ? p.record_sweeps : 0;
+    r.record_count = r.record_sweeps > 0 ? p.record_count : 0;
+    if (r.record_count > 0) {
+      const size_t rcn = (size_t)r.record_count * r.record_sweeps;
+      r.rec_cost.resize(rcn);
+      r.rec_gates.resize(rcn * c.var_doubles);
+      QF_CHECK(cudaMemcpyAsync(r.rec_cost.data(), W + E.L.rec_cost, rcn * 8,
+                               cudaMemcpyDeviceToHost, st));
+      if (c.var_doubles > 0)
+        QF_CHECK(cudaMemcpyAsync(r.rec_gates.data(), W + E.L.rec_gates,
+                                 r.rec_gates.size() * 8, cudaMemcpyDeviceToHost, st));
+      d2h += (long long)(rcn + r.rec_gates.size()) * 8;
+    }
+    QF_CHECK(cudaStreamSynchronize(st));
+    long long ss = 0;
+    int mx = 0;
+    for (const auto &q : r.summary) {
+      ss += q.iters;
+      mx = std::max(mx, q.iters);
+    }
+    // algorithmic bytes: launches of context j moved their bytes for the
+    // n_active(j) starts active then
+    const double ct_bytes = 32.0 * (double)N * (double)N;
+    double sw_b = 0.0, env_b = 0.0, trace_b = 0.0;
+    long long sw_n = 0, env_n = 0;
+    for (int j = 0; j <= last && j < (int)E.sw_ctx.size(); j++) {
+      const double na = (double)h_nact[j];
+      sw_b += na * ct_bytes * (double)E.sw_ctx[j];
+      env_b += na * (double)E.env_bytes_ctx[j];
+      sw_n += E.sw_ctx[j];
+      env_n += E.env_ctx[j];
+      if (j < last) trace_b += na * 16.0 * N;
+    }
+    E.prof.drain();
+    r.stats.alg_bytes_total = sw_b + env_b + trace_b + (double)S * 16.0 * N * N;  // + V^dagger copy
+    r.stats.sandwich_bytes = sw_b;
+    r.stats.env_bytes = env_b;
+    r.stats.sandwich_launches = sw_n;
+    r.stats.env_launches = env_n;
+    r.stats.sandwich_ms = E.prof.ms[0];
+    r.stats.env_ms = E.prof.ms[1];
+    r.stats.kernel_launches = E.launches;
+    r.stats.sweeps = mx;
+    r.stats.engine = QF_ENGINE_STREAM;
+    r.stats.start_sweeps = ss;
+    r.stats.h2d_bytes += h2d;
+    r.stats.d2h_bytes += d2h;
+  } else {
+    QF_CHECK(cudaStreamSynchronize(st));
+  }
+  return QF_OK;
+}
+
+qf_status select_best_device(const qf_summary *d, long long count, cudaStream_t st,
+                             long long *d_best) {
+  k_select_best<<<1, 1024, 0, st>>>(d, count, d_best);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "k_select_best");
+  return QF_OK;
+}
+
+}  // namespace qf

@@ -1,0 +1,561 @@
+// qf_kernels.cuh -- sm_100a kernels of the QFactor multi-start sweep, complex fp64.
+//
+// arXiv 2306.08152 Alg. 1, re-designed for B200:
+//   k_sandwich   fused peel + re-apply of one gate over every active start's
+//                circuit tensor: ct <- E(L) ct E(R)  (one HBM read + write of
+//                ct per gate step; peel identity DESIGN.md).
+//                Also the one-sided InitCircuitTensor pass (R absent).
+//   k_env_polar  partial-trace environment and the
+//                polar/SVD update u_new = Y X^dagger (eq:opt_u), one
+//                warp per start: fixed-order shuffle reductions + a parallel-
+//                ordered one-sided Jacobi in warp shared memory.
+//   k_trace_mask Tr(ct), Delta = 1 - |Tr|/N, the per-start termination
+//                state machine and the parity records.
+//   k_compact    stable compaction of the active-start list (1 CTA).
+//
+// Conventions as in include/qf.h.  double2 = (re, im).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qf {
+
+constexpr int kMaxQubits = 12;
+constexpr int kTileItems = 256;   // work items per sandwich tile (= threads)
+constexpr int kScratch = 64;      // complex per start in the u_old scratch
+
+// ------------------------------------------------------------------ bits
+// Bit bookkeeping of one gate on n qubits.  Local index a of a gate at
+// location loc[0..m): bit (m-1-t) of a <-> basis bit pos[t] = n-1-loc[t].
+struct Bits {
+  int n, m, d;
+  int abits[8];            // basis-bit pattern of local index a
+  int rest_pos[kMaxQubits];// ascending basis-bit positions not in the location
+};
+
+__device__ __forceinline__ int spread_rest(const Bits &B, int r) {
+  int x = 0;
+  const int k_end = B.n - B.m;
+  for (int k = 0; k < k_end; k++) x |= ((r >> k) & 1) << B.rest_pos[k];
+  return x;
+}
+
+// ------------------------------------------------------------------ complex
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// acc + a*b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+// acc + conj(a)*b
+__device__ __forceinline__ double2 cfma_cj(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) {
+  return make_double2(a.x * s, a.y * s);
+}
+__device__ __forceinline__ double cabs2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
+// ------------------------------------------------------------------ sandwich
+// One launch = one gate step over all active starts.  Tile of one start:
+// rows {ins(a, r) : a < d, r0 <= r < r0+RT}, columns {ins(b, c) : b < d,
+// c0 <= c < c0+CT}; the DC = d*CT tile columns are the basis columns whose
+// bits at col_dep[0..log_dc) vary (ascending positions, so consecutive
+// threads touch consecutive 16-byte elements).
+struct SandwichArgs {
+  Bits b;
+  int N;
+  double2 *ct;
+  long long ct_stride;          // N*N
+  const int *active;
+  const int *n_active;
+  const double2 *lsrc;          // left operand of start s at lsrc + s*lstride
+  long long lstride;
+  int ldag;
+  const double2 *rsrc;          // right operand (nullptr: none)
+  long long rstride;
+  int rdag;
+  int DC, CT, RT, TC, tiles_per_start;
+  int log_dc, log_ct;
+  int col_dep[kMaxQubits];      // basis column bit of tile-column-index bit k
+  int jt_b[8];                  // tile-column-index pattern of local index b
+  int jt_rest[kMaxQubits];      // tile-column-index bit of low rest bit k
+};
+
+template <int D>
+__global__ void __launch_bounds__(kTileItems)
+    k_sandwich(const SandwichArgs A) {
+  extern __shared__ double2 sm[];
+  double2 *tile = sm;                       // D * kTileItems
+  double2 *Ls = sm + D * kTileItems;        // D*D
+  double2 *Rs = Ls + D * D;                 // D*D
+  const int nact = *A.n_active;
+  const long long total = (long long)nact * A.tiles_per_start;
+  const long long chunk = (total + gridDim.x - 1) / gridDim.x;
+  const long long t0 = (long long)blockIdx.x * chunk;
+  const long long t1 = t0 + chunk < total ? t0 + chunk : total;
+  const int tid = threadIdx.x;
+  const int items = A.RT * A.DC;
+  const bool has_r = A.rsrc != nullptr;
+  const int N = A.N;
+
+  // phase-1/3 item of this thread: tile row-rest rl1, tile column jt1
+  const int rl1 = tid / A.DC, jt1 = tid - (tid / A.DC) * A.DC;
+  int col1 = 0;
+  for (int k = 0; k < A.log_dc; k++) col1 |= ((jt1 >> k) & 1) << A.col_dep[k];
+  const int row1 = spread_rest(A.b, rl1);
+  // phase-2 item: tile row-rest rl2 (= rl1), row a2, tile column-rest cl2
+  const int a2 = (tid / A.CT) % D, cl2 = tid % A.CT;
+  int jt_c2 = 0;
+  for (int k = 0; k < A.log_ct; k++) jt_c2 |= ((cl2 >> k) & 1) << A.jt_rest[k];
+
+  int cur = -1;
+  for (long long t = t0; t < t1; t++) {
+    const int ai = (int)(t / A.tiles_per_start);
+    const int tt = (int)(t - (long long)ai * A.tiles_per_start);
+    const int s = A.active[ai];
+    if (s != cur) {  // CTA-uniform branch
+      __syncthreads();  // previous tile done with Ls / Rs
+      if (tid < D * D) {
+        const double2 *L = A.lsrc + (long long)s * A.lstride;
+        const int i = tid / D, j = tid % D;
+        Ls[tid] = A.ldag ? cconj(L[j * D + i]) : L[tid];
+        if (has_r) {
+          const double2 *R = A.rsrc + (long long)s * A.rstride;
+          Rs[tid] = A.rdag ? cconj(R[j * D + i]) : R[tid];
+        }
+      }
+      cur = s;
+      __syncthreads();
+    }
+    const int tr = tt / A.TC, tc = tt - (tt / A.TC) * A.TC;
+    const int rbase = spread_rest(A.b, tr * A.RT) | row1;
+    const int cbase = spread_rest(A.b, tc * A.CT) | col1;
+    double2 *cts = A.ct + (long long)s * A.ct_stride;
+    if (tid < items) {
+      double2 x[D];
+#pragma unroll
+      for (int a = 0; a < D; a++)
+        x[a] = cts[(long long)(rbase | A.b.abits[a]) * N + cbase];
+      double2 y[D];
+#pragma unroll
+      for (int a = 0; a < D; a++) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k], acc);
+        y[a] = acc;
+      }
+      if (has_r) {
+#pragma unroll
+        for (int a = 0; a < D; a++) tile[(rl1 * D + a) * A.DC + jt1] = y[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < D; a++)
+          cts[(long long)(rbase | A.b.abits[a]) * N + cbase] = y[a];
+      }
+    }
+    if (has_r) {
+      __syncthreads();
+      if (tid < items) {
+        double2 *base = tile + (rl1 * D + a2) * A.DC;
+        double2 z[D];
+#pragma unroll
+        for (int b = 0; b < D; b++) z[b] = base[jt_c2 | A.jt_b[b]];
+#pragma unroll
+        for (int b = 0; b < D; b++) {
+          double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < D; k++) acc = cfma(z[k], Rs[k * D + b], acc);
+          base[jt_c2 | A.jt_b[b]] = acc;
+        }
+      }
+      __syncthreads();
+      if (tid < items) {
+#pragma unroll
+        for (int a = 0; a < D; a++)
+          cts[(long long)(rbase | A.b.abits[a]) * N + cbase] =
+              tile[(rl1 * D + a) * A.DC + jt1];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ env + polar
+struct EnvArgs {
+  Bits b;
+  int N;
+  const double2 *ct;
+  long long ct_stride;
+  const int *active;
+  const int *n_active;
+  double2 *gates;       // packed gates, start s at gates + s*gstride
+  long long gstride;    // complex per start
+  int goff;             // complex offset of this gate
+  double2 *scratch;     // u_old copy, kScratch complex per start
+  int forward;          // 0: backward half, 1: forward half
+  double beta;
+};
+
+// Round-robin (circle method) pairing for a parallel-ordered Jacobi sweep:
+// round rd, pair p -> columns (cp < cq).  Every pair of columns meets once
+// per sweep of D-1 rounds.
+template <int D>
+__device__ __forceinline__ void rr_pair(int rd, int p, int &cp, int &cq) {
+  auto player = [&](int k) { return k == 0 ? 0 : 1 + ((k - 1 + rd) % (D - 1)); };
+  const int x = player(p), y = player(D - 1 - p);
+  cp = x < y ? x : y;
+  cq = x < y ? y : x;
+}
+
+// Unitary polar factor of A (D x D, warp shared memory) into U; V, W scratch.
+// One-sided Jacobi: rotate column pairs of A (and of V = I) until the columns
+// are orthogonal, A V = X diag(sigma); then pf(A) = X V^dagger.
+template <int D>
+__device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane) {
+  if constexpr (D == 2) {
+    if (lane == 0) {
+      const double2 a = Am[0], b = Am[1], c = Am[2], e = Am[3];
+      const double2 det = make_double2(a.x * e.x - a.y * e.y - (b.x * c.x - b.y * c.y),
+                                       a.x * e.y + a.y * e.x - (b.x * c.y + b.y * c.x));
+      const double adet = hypot(det.x, det.y);
+      const double2 ph = adet > 0.0 ? make_double2(det.x / adet, det.y / adet)
+                                    : make_double2(1.0, 0.0);
+      const double nrm = sqrt(cabs2(a) + cabs2(b) + cabs2(c) + cabs2(e) + 2.0 * adet);
+      if (nrm > 0.0) {
+        const double inv = 1.0 / nrm;
+        // adj(A)^H = [[conj e, -conj c], [-conj b, conj a]]
+        U[0] = cscale(cadd(a, cmul(ph, cconj(e))), inv);
+        U[1] = cscale(cadd(b, cmul(ph, make_double2(-c.x, c.y))), inv);
+        U[2] = cscale(cadd(c, cmul(ph, make_double2(-b.x, b.y))), inv);
+        U[3] = cscale(cadd(e, cmul(ph, cconj(a))), inv);
+      } else {
+        U[0] = make_double2(1.0, 0.0);
+        U[1] = make_double2(0.0, 0.0);
+        U[2] = make_double2(0.0, 0.0);
+        U[3] = make_double2(1.0, 0.0);
+      }
+    }
+    __syncwarp();
+  } else {
+  for (int e = lane; e < D * D; e += 32)
+    Vm[e] = make_double2(e / D == e % D ? 1.0 : 0.0, 0.0);
+  __syncwarp();
+  const int p = lane / D, i = lane % D;
+  const bool act = p < D / 2;
+  for (int sweep = 0; sweep < 40; sweep++) {
+    bool any = false;
+    for (int rd = 0; rd < D - 1; rd++) {
+      int cp = 0, cq = 1;
+      if (act) rr_pair<D>(rd, p, cp, cq);
+      double2 ap = make_double2(0, 0), aq = ap, vp = ap, vq = ap;
+      double al = 0.0, be = 0.0;
+      double2 ga = make_double2(0.0, 0.0);
+      if (act) {
+        ap = Am[i * D + cp];
+        aq = Am[i * D + cq];
+        vp = Vm[i * D + cp];
+        vq = Vm[i * D + cq];
+        al = cabs2(ap);
+        be = cabs2(aq);
+        ga = cfma_cj(ap, aq, ga);
+      }
+#pragma unroll
+      for (int off = 1; off < D; off <<= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, off);
+        be += __shfl_xor_sync(0xffffffffu, be, off);
+        ga.x += __shfl_xor_sync(0xffffffffu, ga.x, off);
+        ga.y += __shfl_xor_sync(0xffffffffu, ga.y, off);
+      }
+      const double g = sqrt(cabs2(ga));
+      const bool rot = act && g > 0.0 && g > 1e-15 * sqrt(al * be);
+      if (rot) {
+        // e^{-i phi} = conj(gamma)/|gamma| makes the 2x2 Gram real; then the
+        // symmetric Schur rotation (Golub & Van Loan 8.4.1).
+        const double2 ph = make_double2(ga.x / g, -ga.y / g);
+        const double zeta = (be - al) / (2.0 * g);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        const double2 aq2 = cmul(aq, ph), vq2 = cmul(vq, ph);
+        Am[i * D + cp] = make_double2(c * ap.x - s * aq2.x, c * ap.y - s * aq2.y);
+        Am[i * D + cq] = make_double2(s * ap.x + c * aq2.x, s * ap.y + c * aq2.y);
+        Vm[i * D + cp] = make_double2(c * vp.x - s * vq2.x, c * vp.y - s * vq2.y);
+        Vm[i * D + cq] = make_double2(s * vp.x + c * vq2.x, s * vp.y + c * vq2.y);
+      }
+      any |= __any_sync(0xffffffffu, rot);
+      __syncwarp();
+    }
+    if (!any) break;
+  }
+  // column norms -> X = A V / sigma (in place in Am)
+  double sig = 0.0;
+  if (lane < D) {
+    for (int r = 0; r < D; r++) sig += cabs2(Am[r * D + lane]);
+    sig = sqrt(sig);
+  }
+  double smax = sig;
+  for (int off = 16; off > 0; off >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, off));
+  const bool ok = lane >= D || (sig > 1e-13 * smax && sig > 0.0);
+  const unsigned deficient = __ballot_sync(0xffffffffu, !ok);
+  __syncwarp();
+  if (lane < D && ok) {
+    const double inv = 1.0 / sig;
+    for (int r = 0; r < D; r++) Am[r * D + lane] = cscale(Am[r * D + lane], inv);
+  }
+  __syncwarp();
+  if (deficient && lane == 0) {
+    // rank-deficient environment: complete the deficient columns
+    // of X by Gram-Schmidt over e_0, e_1, ... against the good columns.
+    for (int j = 0; j < D; j++) {
+      if (!((deficient >> j) & 1)) continue;
+      for (int e = 0; e < D; e++) {
+        double2 v[D];
+        for (int r = 0; r < D; r++) v[r] = make_double2(r == e ? 1.0 : 0.0, 0.0);
+        for (int pass = 0; pass < 2; pass++)
+          for (int k = 0; k < D; k++) {
+            if (k == j || (((deficient >> k) & 1) && k > j)) continue;
+            double2 dot = make_double2(0.0, 0.0);
+            for (int r = 0; r < D; r++) dot = cfma_cj(Am[r * D + k], v[r], dot);
+            for (int r = 0; r < D; r++) {
+              const double2 pr = cmul(dot, Am[r * D + k]);
+              v[r] = make_double2(v[r].x - pr.x, v[r].y - pr.y);
+            }
+          }
+        double nn = 0.0;
+        for (int r = 0; r < D; r++) nn += cabs2(v[r]);
+        nn = sqrt(nn);
+        if (nn > 0.5) {
+          for (int r = 0; r < D; r++) Am[r * D + j] = cscale(v[r], 1.0 / nn);
+          break;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // U = X V^dagger
+  for (int o = lane; o < D * D; o += 32) {
+    const int r = o / D, c = o % D;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      const double2 x = Am[r * D + k], v = Vm[c * D + k];
+      // x * conj(v)
+      acc.x = fma(x.x, v.x, acc.x);
+      acc.x = fma(x.y, v.y, acc.x);
+      acc.y = fma(x.y, v.x, acc.y);
+      acc.y = fma(-x.x, v.y, acc.y);
+    }
+    U[o] = acc;
+  }
+  __syncwarp();
+  }  // D > 2
+}
+
+constexpr int kEnvWarps = 4;
+
+template <int D>
+__global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
+  __shared__ double2 smem[kEnvWarps][4 * D * D];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2 *Uo = smem[w];
+  double2 *Pm = Uo + D * D;
+  double2 *Am = Pm + D * D;
+  double2 *Vm = Am + D * D;
+  const int nact = *A.n_active;
+  constexpr int DD = D * D;
+  constexpr int SPLIT = DD >= 32 ? 1 : 32 / DD;  // lanes per output
+  constexpr int OPL = DD >= 32 ? DD / 32 : 1;    // outputs per lane
+  const int R = 1 << (A.b.n - A.b.m);
+  const int N = A.N;
+  for (int ai = blockIdx.x * kEnvWarps + w; ai < nact; ai += gridDim.x * kEnvWarps) {
+    const int s = A.active[ai];
+    double2 *u = A.gates + (long long)s * A.gstride + A.goff;
+    for (int e = lane; e < DD; e += 32) Uo[e] = u[e];
+    // P = PT(ct): P[a][b] = sum_r ct[ins(a,r)][ins(b,r)], r ascending per lane
+    const double2 *cts = A.ct + (long long)s * A.ct_stride;
+    const int k = lane % SPLIT;
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {
+      const int o = (lane / SPLIT) + q * (32 / SPLIT);
+      const int a = o / D, b = o % D;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int r = k; r < R; r += SPLIT) {
+        const int sp = spread_rest(A.b, r);
+        const double2 v = cts[(long long)(sp | A.b.abits[a]) * N + (sp | A.b.abits[b])];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+#pragma unroll
+      for (int off = 1; off < SPLIT; off <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      }
+      if (k == 0) Pm[o] = acc;
+    }
+    __syncwarp();
+    // A = E^dagger with E = (1-beta) PT(peeled ct) + beta u_old^dagger:
+    //   backward: E0 = u_old^dagger P  ->  E0^dagger = P^dagger u_old
+    //   forward : E0 = P u_old^dagger  ->  E0^dagger = u_old P^dagger
+    for (int o = lane; o < DD; o += 32) {
+      const int r = o / D, c = o % D;
+      double2 acc = make_double2(0.0, 0.0);
+      if (!A.forward) {
+#pragma unroll
+        for (int kk = 0; kk < D; kk++) acc = cfma_cj(Pm[kk * D + r], Uo[kk * D + c], acc);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < D; kk++) {
+          const double2 x = Uo[r * D + kk], pv = Pm[c * D + kk];
+          acc.x = fma(x.x, pv.x, acc.x);
+          acc.x = fma(x.y, pv.y, acc.x);
+          acc.y = fma(x.y, pv.x, acc.y);
+          acc.y = fma(-x.x, pv.y, acc.y);
+        }
+      }
+      if (A.beta != 0.0) {
+        acc = cscale(acc, 1.0 - A.beta);
+        acc.x = fma(A.beta, Uo[o].x, acc.x);
+        acc.y = fma(A.beta, Uo[o].y, acc.y);
+      }
+      Am[o] = acc;
+    }
+    __syncwarp();
+    warp_polar<D>(Am, Vm, Pm, lane);
+    double2 *sc = A.scratch + (long long)s * kScratch;
+    for (int e = lane; e < DD; e += 32) {
+      sc[e] = Uo[e];
+      u[e] = Pm[e];
+    }
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ trace + mask
+struct TraceArgs {
+  int N;
+  const double2 *ct;
+  long long ct_stride;
+  const int *active;
+  const int *n_active;
+  int it;  // sweep just completed (1-based); 0 = max_iters == 0 call
+  double dist_tol, diff_tol_a, diff_tol_r, long_diff_r;
+  int long_diff_count, min_iters, max_iters, ring;
+  double *hist;   // S x ring
+  double *delta;
+  int *iters;
+  int *verdict;
+  const int *rec_slot;  // S, -1 = not recorded
+  int R;
+  double *rec_cost;     // slots x R
+  double *rec_gates;    // slots x R x var
+  const double *gates;  // S x var (doubles)
+  int var_doubles;
+};
+
+constexpr int kTraceWarps = 8;
+
+__global__ void __launch_bounds__(32 * kTraceWarps) k_trace_mask(const TraceArgs A) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nact = *A.n_active;
+  for (int ai = blockIdx.x * kTraceWarps + w; ai < nact; ai += gridDim.x * kTraceWarps) {
+    const int s = A.active[ai];
+    const double2 *cts = A.ct + (long long)s * A.ct_stride;
+    double re = 0.0, im = 0.0;
+    for (int i = lane; i < A.N; i += 32) {
+      const double2 v = cts[(long long)i * A.N + i];
+      re += v.x;
+      im += v.y;
+    }
+    for (int off = 1; off < 32; off <<= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, off);
+      im += __shfl_xor_sync(0xffffffffu, im, off);
+    }
+    const double c = 1.0 - hypot(re, im) / (double)A.N;
+    const int it = A.it;
+    if (lane == 0) {
+      int v = 0;
+      if (it == 0) {
+        v = 4;  // QF_MAX_ITER with the initial Delta
+      } else {
+        double *h = A.hist + (long long)s * A.ring;
+        h[it % A.ring] = c;
+        if (!isfinite(c)) {
+          v = 5;
+        } else {
+          if (it >= A.min_iters) {
+            const int L = A.long_diff_count;
+            if (c <= A.dist_tol) {
+              v = 1;
+            } else if (it >= 2 && fabs(c - h[(it - 1) % A.ring]) <= A.diff_tol_a + A.diff_tol_r * c) {
+              v = 2;
+            } else if (L > 0 && it > L) {
+              const double cl = h[(it - L) % A.ring];
+              if (cl - c <= A.long_diff_r * cl) v = 3;
+            }
+          }
+          if (v == 0 && it >= A.max_iters) v = 4;
+        }
+      }
+      A.delta[s] = c;
+      A.iters[s] = it;
+      A.verdict[s] = v;
+    }
+    if (A.R > 0 && it >= 1 && it <= A.R) {
+      const int slot = A.rec_slot[s];
+      if (slot >= 0) {
+        if (lane == 0) A.rec_cost[(long long)slot * A.R + it - 1] = c;
+        const double *g = A.gates + (long long)s * A.var_doubles;
+        double *dst = A.rec_gates + ((long long)slot * A.R + it - 1) * A.var_doubles;
+        for (int e = lane; e < A.var_doubles; e += 32) dst[e] = g[e];
+      }
+    }
+  }
+}
+
+// Stable in-place compaction of the active list: keep starts still RUNNING.
+__global__ void __launch_bounds__(1024) k_compact(int *active, int *n_active, const int *verdict) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int n = *n_active;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int chunk = 0; chunk < n; chunk += 1024) {
+    const int idx = chunk + tid;
+    const int s = idx < n ? active[idx] : -1;
+    const int keep = (s >= 0 && verdict[s] == 0) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    const int wpre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int k = 0; k < 32; k++) {
+      const int v = wsum[k];
+      off += k < w ? v : 0;
+      tot += v;
+    }
+    const int b0 = base;
+    __syncthreads();
+    if (keep) active[b0 + off + wpre] = s;
+    __syncthreads();
+    if (tid == 0) base = b0 + tot;
+    __syncthreads();
+  }
+  if (tid == 0) *n_active = base;
+}
+
+}  // namespace qf
