@@ -15,6 +15,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "qf_internal.h"
@@ -25,6 +27,7 @@ namespace qf {
 namespace {
 
 constexpr int kRingMin = 2;
+constexpr int kRowsMaxQubits = 9;
 
 // CUDA-event timing of individual launches (qf_params.profile = 1): a ring of
 // event pairs, harvested when a slot is reused and at the end of the call.
@@ -194,10 +197,22 @@ __global__ void __launch_bounds__(1024) k_select_best(const qf_summary *q, long 
 // ------------------------------------------------------------------ host helpers
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+// row-tile geometry of k_sandwich_rows for arity m on n qubits: (RT, tiles/start)
+std::pair<int, int> row_tiles(int n, int m) {
+  const int N = 1 << n, D = 1 << m;
+  const int target = D == 8 ? 2048 : 1024;  // elements per tile
+  const int RT = std::max(1, std::min(N / D, target / (D * N)));
+  return {RT, (N / D) / RT};
+}
+
 struct Layout {
   size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
-      rec_slot, rec_starts, rec_cost, rec_gates, summary, best, total;
+      rec_slot, rec_starts, rec_cost, rec_gates, summary, best, part, tpart, vstore, vslots,
+      total;
+  long long vstride;  // complex per start in vstore (sum over VARIABLE gates of 2 d^2)
+  int nvslots;
   int ring;
+  int max_parts;  // tiles per start of the row-tile sandwich (fused partials), 0 = unused
 };
 
 Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
@@ -229,6 +244,20 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
   L.rec_gates = take(std::max<size_t>(1, rc * R * (size_t)c.var_doubles) * 8);
   L.summary = take(S * sizeof(qf_summary));
   L.best = take(16);
+  L.max_parts = 0;
+  if (c.n <= kRowsMaxQubits)
+    for (int k = 0; k < c.p; k++) L.max_parts = std::max(L.max_parts, row_tiles(c.n, c.arity[k]).second);
+  L.part = take(std::max<size_t>(1, S * (size_t)L.max_parts * 64) * 16);
+  L.tpart = take(std::max<size_t>(1, S * (size_t)L.max_parts) * 16);
+  L.vstride = 0;
+  L.nvslots = 0;
+  for (int k = 0; k < c.p; k++)
+    if (c.kind[k] == QF_GATE_VARIABLE) {
+      L.vstride += 2LL << (2 * c.arity[k]);
+      L.nvslots += 2;
+    }
+  L.vstore = take(std::max<size_t>(1, S * (size_t)L.vstride) * 16);
+  L.vslots = take((size_t)std::max(1, L.nvslots) * 8);
   L.total = o;
   return L;
 }
@@ -296,6 +325,9 @@ struct Engine {
   char *ws;
   Layout L;
   int S, N, nsm = 148;
+  bool use_rows = true;  // QF_SANDWICH=tile forces the register-tile kernel (A/B runs)
+  bool warm = true;      // QF_WARM=0 disables the warm-started Jacobi (A/B runs)
+  std::vector<int> voff; // per gate: complex offset of its backward slot in vstore
   long long launches = 0;
   int sandwich_grid[4] = {0, 0, 0, 0};
   // byte accounting: launches per "context" j; the active count in context j
@@ -321,6 +353,15 @@ struct Engine {
     env_ctx.assign((size_t)p.max_iters + 2, 0);
     env_bytes_ctx.assign((size_t)p.max_iters + 2, 0);
     if (p.profile) prof.init();
+    if (const char *e = getenv("QF_SANDWICH")) use_rows = std::string(e) != "tile";
+    if (const char *e = getenv("QF_WARM")) warm = std::string(e) != "0";
+    voff.assign(c.p, -1);
+    long long o = 0;
+    for (int k = 0; k < c.p; k++)
+      if (c.kind[k] == QF_GATE_VARIABLE) {
+        voff[k] = (int)o;
+        o += 2LL << (2 * c.arity[k]);
+      }
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -346,7 +387,81 @@ struct Engine {
     return cudaGetLastError();
   }
 
+  // TMA row-tile pipeline (n <= kRowsMaxQubits) -- see k_sandwich_rows
+  int rows_grid[4][5] = {};
+  template <int D>
+  cudaError_t launch_rows(const SandwichArgs &SA) {
+    RowTileArgs A{};
+    A.b = SA.b;
+    A.N = N;
+    A.ct = SA.ct;
+    A.ct_stride = SA.ct_stride;
+    A.active = SA.active;
+    A.n_active = SA.n_active;
+    A.lsrc = SA.lsrc;
+    A.lstride = SA.lstride;
+    A.ldag = SA.ldag;
+    A.rsrc = SA.rsrc;
+    A.rstride = SA.rstride;
+    A.rdag = SA.rdag;
+    const auto rt = row_tiles(c.n, A.b.m);
+    A.RT = rt.first;
+    A.tiles_per_start = rt.second;
+    const size_t tile_bytes = (size_t)A.RT * D * N * 16;
+    A.stages = (int)std::max<size_t>(2, std::min<size_t>(4, (96 * 1024) / tile_bytes));
+    const size_t smem = A.stages * tile_bytes + 2 * D * D * 16 + 2 * A.stages * 8 + 2 * kMaxTileRows * 4;
+    // fused epilogue for the next step
+    if (next_k >= 0) {
+      const Bits nb = make_bits(c, next_k);
+      A.nx_env = 1;
+      A.nd = nb.d;
+      A.nmask = nb.abits[nb.d - 1];
+      for (int a = 0; a < nb.d; a++) A.nab[a] = nb.abits[a];
+      A.part = reinterpret_cast<double2 *>(ws + L.part);
+      A.part_stride = (long long)L.max_parts * 64;
+      part_k = next_k;
+      part_dir = next_dir;
+      part_tiles = A.tiles_per_start;
+    }
+    if (next_trace) {
+      A.nx_trace = 1;
+      A.tpart = reinterpret_cast<double2 *>(ws + L.tpart);
+      A.tpart_stride = L.max_parts;
+      tpart_tiles = A.tiles_per_start;
+    }
+    int &grid = rows_grid[ilog2(D)][A.stages];
+    if (grid == 0) {
+      cudaFuncSetAttribute(k_sandwich_rows<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sandwich_rows<D>, kRowThreads + 32,
+                                                    smem);
+      grid = std::max(1, per_sm) * nsm;
+    }
+    const long long total = (long long)S * A.tiles_per_start;
+    const int g = (int)std::max<long long>(1, std::min<long long>(grid, total));
+    const int slot = prof.on ? prof.open(0, st) : -1;
+    k_sandwich_rows<D><<<g, kRowThreads + 32, smem, st>>>(A);
+    if (slot >= 0) prof.close(slot, st);
+    launches++;
+    sw_ctx[ctx]++;
+    return cudaGetLastError();
+  }
+
+  // next step of the schedule whose inputs the row-tile epilogue produces
+  int next_k = -1, next_dir = 0;
+  bool next_trace = false;
+  // fused partials available for env(part_k, part_dir) / the trace
+  int part_k = -1, part_dir = 0, part_tiles = 0, tpart_tiles = 0;
+
   cudaError_t sandwich(const SandwichArgs &A) {
+    if (use_rows && c.n <= kRowsMaxQubits && row_tiles(c.n, A.b.m).first * A.b.d <= 32) {
+      switch (A.b.d) {
+        case 2: return launch_rows<2>(A);
+        case 4: return launch_rows<4>(A);
+        default: return launch_rows<8>(A);
+      }
+    }
     switch (A.b.d) {
       case 2: return launch_sandwich<2>(A);
       case 4: return launch_sandwich<4>(A);
@@ -380,6 +495,17 @@ struct Engine {
     A.scratch = scratch();
     A.forward = forward;
     A.beta = p.beta;
+    if (warm) {
+      A.vstore = reinterpret_cast<double2 *>(ws + L.vstore);
+      A.vstride = L.vstride;
+      A.voff = voff[k] + (forward ? A.b.d * A.b.d : 0);
+    }
+    if (part_k == k && part_dir == forward) {
+      A.part = reinterpret_cast<const double2 *>(ws + L.part);
+      A.part_stride = (long long)L.max_parts * 64;
+      A.part_tiles = part_tiles;
+    }
+    part_k = -1;
     switch (A.b.d) {
       case 2: return launch_env<2>(A);
       case 4: return launch_env<4>(A);
@@ -422,6 +548,19 @@ struct Engine {
     cudaError_t e = cudaSuccess;
     if (c.kind[k] == QF_GATE_VARIABLE && (e = env(k, forward)) != cudaSuccess) return e;
     SandwichArgs A = base_args(k);
+    // the schedule's next step: backward k-1 ... 0, then forward 0 ... p-1,
+    // then (after the cost) the next sweep's backward p-1
+    int nk, nd;
+    if (!forward) {
+      nk = k > 0 ? k - 1 : 0;
+      nd = k > 0 ? 0 : 1;
+    } else {
+      nk = k < c.p - 1 ? k + 1 : c.p - 1;
+      nd = k < c.p - 1 ? 1 : 0;
+    }
+    next_k = c.kind[nk] == QF_GATE_VARIABLE ? nk : -1;
+    next_dir = nd;
+    next_trace = forward && k == c.p - 1;
     if (!forward) {  // ct <- E(u_old)^dagger ct E(u_new)
       old_operand(k, A.lsrc, A.lstride);
       A.ldag = 1;
@@ -442,14 +581,28 @@ struct Engine {
     const int g = (int)std::max<long long>(1, std::min<long long>((S * NN + 255) / 256, nsm * 32));
     k_ct_from_vdag<<<g, 256, 0, st>>>(ct(), NN, vdag(), active(), n_active());
     launches++;
+    if (warm && L.nvslots > 0) {  // warm starts restart from I with every (re)build
+      const long long tot = (long long)S * L.nvslots;
+      const int gv = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, nsm * 8));
+      k_vstore_identity<<<gv, 256, 0, st>>>(reinterpret_cast<double2 *>(ws + L.vstore), L.vstride,
+                                            S, reinterpret_cast<const int2 *>(ws + L.vslots),
+                                            L.nvslots);
+      launches++;
+    }
     cudaError_t e = cudaGetLastError();
     for (int k = 0; k < c.p && e == cudaSuccess; k++) {
       SandwichArgs A = base_args(k);
       gate_operand(k, A.lsrc, A.lstride);
       A.ldag = 0;
       A.rsrc = nullptr;
+      // the last pass produces the inputs of the first sweep step (backward p-1)
+      next_k = (k == c.p - 1 && c.kind[k] == QF_GATE_VARIABLE) ? k : -1;
+      next_dir = 0;
+      next_trace = false;
       e = sandwich(A);
     }
+    next_k = -1;
+    next_trace = false;
     return e;
   }
 
@@ -479,6 +632,12 @@ struct Engine {
     A.rec_gates = reinterpret_cast<double *>(ws + L.rec_gates);
     A.gates = gates();
     A.var_doubles = c.var_doubles;
+    if (tpart_tiles > 0 && it > 0) {
+      A.tpart = reinterpret_cast<const double2 *>(ws + L.tpart);
+      A.tpart_stride = L.max_parts;
+      A.tpart_tiles = tpart_tiles;
+    }
+    tpart_tiles = 0;
     const int g = std::max(1, std::min((S + kTraceWarps - 1) / kTraceWarps, nsm * 8));
     k_trace_mask<<<g, 32 * kTraceWarps, 0, st>>>(A);
     launches++;
@@ -527,6 +686,18 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     QF_CHECK(cudaMemcpyAsync(W + E.L.gtab, tab.data(), tab.size() * sizeof(int2),
                              cudaMemcpyHostToDevice, st));
     h2d += (long long)(tab.size() * sizeof(int2));
+  }
+  std::vector<int2> vslots;
+  for (int k = 0; k < c.p; k++)
+    if (c.kind[k] == QF_GATE_VARIABLE) {
+      const int d = 1 << c.arity[k];
+      vslots.push_back(make_int2(E.voff[k], d));
+      vslots.push_back(make_int2(E.voff[k] + d * d, d));
+    }
+  if (!vslots.empty()) {
+    QF_CHECK(cudaMemcpyAsync(W + E.L.vslots, vslots.data(), vslots.size() * sizeof(int2),
+                             cudaMemcpyHostToDevice, st));
+    h2d += (long long)(vslots.size() * sizeof(int2));
   }
   QF_CHECK(cudaMemsetAsync(E.bad(), 0, sizeof(int), st));
   const int g1 = std::max(1, std::min((int)(((long long)N * N + 255) / 256), E.nsm * 8));

@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "qf_ptx.cuh"
+
 namespace qf {
 
 constexpr int kMaxQubits = 12;
@@ -209,6 +211,12 @@ struct EnvArgs {
   double2 *scratch;     // u_old copy, kScratch complex per start
   int forward;          // 0: backward half, 1: forward half
   double beta;
+  const double2 *part;  // fused partials from the previous sandwich (nullptr: gather)
+  long long part_stride;
+  int part_tiles;
+  double2 *vstore;      // warm-start right singular vectors (nullptr: cold Jacobi)
+  long long vstride;    // complex per start
+  int voff;             // complex offset of (gate, direction)
 };
 
 // Round-robin (circle method) pairing for a parallel-ordered Jacobi sweep:
@@ -225,8 +233,13 @@ __device__ __forceinline__ void rr_pair(int rd, int p, int &cp, int &cq) {
 // Unitary polar factor of A (D x D, warp shared memory) into U; V, W scratch.
 // One-sided Jacobi: rotate column pairs of A (and of V = I) until the columns
 // are orthogonal, A V = X diag(sigma); then pf(A) = X V^dagger.
+// v0 (optional, global): a warm start -- the right singular vectors found the
+// last time this gate was updated in this direction.  Jacobi then runs on
+// A v0 with V = v0, which is already nearly column-orthogonal once the
+// optimisation settles; the polar factor is unique, so only rounding differs.
 template <int D>
-__device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane) {
+__device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
+                           const double2 *v0 = nullptr) {
   if constexpr (D == 2) {
     if (lane == 0) {
       const double2 a = Am[0], b = Am[1], c = Am[2], e = Am[3];
@@ -252,8 +265,22 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane) {
     }
     __syncwarp();
   } else {
-  for (int e = lane; e < D * D; e += 32)
-    Vm[e] = make_double2(e / D == e % D ? 1.0 : 0.0, 0.0);
+  if (v0) {
+    for (int e = lane; e < D * D; e += 32) Vm[e] = v0[e];
+    __syncwarp();
+    for (int o = lane; o < D * D; o += 32) {
+      const int r = o / D, c = o % D;
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < D; k++) acc = cfma(Am[r * D + k], Vm[k * D + c], acc);
+      U[o] = acc;
+    }
+    __syncwarp();
+    for (int o = lane; o < D * D; o += 32) Am[o] = U[o];
+  } else {
+    for (int e = lane; e < D * D; e += 32)
+      Vm[e] = make_double2(e / D == e % D ? 1.0 : 0.0, 0.0);
+  }
   __syncwarp();
   const int p = lane / D, i = lane % D;
   const bool act = p < D / 2;
@@ -385,6 +412,19 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
     const int s = A.active[ai];
     double2 *u = A.gates + (long long)s * A.gstride + A.goff;
     for (int e = lane; e < DD; e += 32) Uo[e] = u[e];
+    if (A.part) {
+      // P = sum over the producing sandwich's tiles, tile order
+      const double2 *pp = A.part + (long long)s * A.part_stride;
+      for (int o = lane; o < DD; o += 32) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int t = 0; t < A.part_tiles; t++) {
+          const double2 v = pp[t * DD + o];
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        Pm[o] = acc;
+      }
+    } else {
     // P = PT(ct): P[a][b] = sum_r ct[ins(a,r)][ins(b,r)], r ascending per lane
     const double2 *cts = A.ct + (long long)s * A.ct_stride;
     const int k = lane % SPLIT;
@@ -405,6 +445,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
       }
       if (k == 0) Pm[o] = acc;
+    }
     }
     __syncwarp();
     // A = E^dagger with E = (1-beta) PT(peeled ct) + beta u_old^dagger:
@@ -434,7 +475,10 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
       Am[o] = acc;
     }
     __syncwarp();
-    warp_polar<D>(Am, Vm, Pm, lane);
+    double2 *vs = A.vstore ? A.vstore + (long long)s * A.vstride + A.voff : nullptr;
+    warp_polar<D>(Am, Vm, Pm, lane, vs);
+    if (vs)
+      for (int e = lane; e < DD; e += 32) vs[e] = Vm[e];
     double2 *sc = A.scratch + (long long)s * kScratch;
     for (int e = lane; e < DD; e += 32) {
       sc[e] = Uo[e];
@@ -464,6 +508,9 @@ struct TraceArgs {
   double *rec_gates;    // slots x R x var
   const double *gates;  // S x var (doubles)
   int var_doubles;
+  const double2 *tpart;  // fused trace partials (nullptr: diagonal gather)
+  long long tpart_stride;
+  int tpart_tiles;
 };
 
 constexpr int kTraceWarps = 8;
@@ -475,14 +522,22 @@ __global__ void __launch_bounds__(32 * kTraceWarps) k_trace_mask(const TraceArgs
     const int s = A.active[ai];
     const double2 *cts = A.ct + (long long)s * A.ct_stride;
     double re = 0.0, im = 0.0;
-    for (int i = lane; i < A.N; i += 32) {
-      const double2 v = cts[(long long)i * A.N + i];
-      re += v.x;
-      im += v.y;
-    }
-    for (int off = 1; off < 32; off <<= 1) {
-      re += __shfl_xor_sync(0xffffffffu, re, off);
-      im += __shfl_xor_sync(0xffffffffu, im, off);
+    if (A.tpart) {
+      const double2 *tp = A.tpart + (long long)s * A.tpart_stride;
+      for (int t = 0; t < A.tpart_tiles; t++) {
+        re += tp[t].x;
+        im += tp[t].y;
+      }
+    } else {
+      for (int i = lane; i < A.N; i += 32) {
+        const double2 v = cts[(long long)i * A.N + i];
+        re += v.x;
+        im += v.y;
+      }
+      for (int off = 1; off < 32; off <<= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, off);
+        im += __shfl_xor_sync(0xffffffffu, im, off);
+      }
     }
     const double c = 1.0 - hypot(re, im) / (double)A.N;
     const int it = A.it;
@@ -556,6 +611,252 @@ __global__ void __launch_bounds__(1024) k_compact(int *active, int *n_active, co
     __syncthreads();
   }
   if (tid == 0) *n_active = base;
+}
+
+}  // namespace qf
+
+// ------------------------------------------------------------------ TMA row-tile sandwich
+// k_sandwich_rows: the same ct <- E(L) ct E(R) step for n <= 9, where a tile is
+// RT*d whole rows of one start {ins(a, r) : a < d, r0 <= r < r0+RT}.  Every
+// row is a contiguous N*16-byte run, so tiles move with TMA bulk copies
+// (cp.async.bulk global->shared with mbarrier completion, and shared->global
+// bulk groups) through a `stages`-deep ring; the CTA computes tile j while
+// the loads of tiles j+1..j+stages-1 and the store of tile j-1 are in flight.
+//   phase 1 (left):  item (rl, column)        mixes the d rows of a column
+//   phase 2 (right): item (rl, a, col-rest c) mixes the d columns ins(b, c)
+// both in place in shared memory.
+namespace qf {
+
+struct RowTileArgs {
+  Bits b;
+  int N;
+  double2 *ct;
+  long long ct_stride;
+  const int *active;
+  const int *n_active;
+  const double2 *lsrc;
+  long long lstride;
+  int ldag;
+  const double2 *rsrc;  // nullptr: one-sided (InitCircuitTensor)
+  long long rstride;
+  int rdag;
+  int RT;               // row-rests per tile
+  int tiles_per_start;  // (N/d)/RT
+  int stages;           // ring depth
+  // fused epilogue for the NEXT step of the schedule (reads the finished tile
+  // in shared memory): partial environment of the next VARIABLE gate,
+  //   part[s][tile][a'*d'+b'] = sum_{tile rows i, i&nmask == nab[a']}
+  //                             ct[i][(i & ~nmask) | nab[b']]
+  // and/or the partial trace tpart[s][tile] = sum_{tile rows i} ct[i][i].
+  int nx_env, nd, nmask;
+  int nab[8];
+  double2 *part;
+  long long part_stride;  // complex per start
+  int nx_trace;
+  double2 *tpart;
+  long long tpart_stride;
+};
+
+constexpr int kRowThreads = 256;
+constexpr int kMaxTileRows = 64;
+
+// Warp-specialised: warps 0..7 compute, warp 8 is the TMA producer.  Lane q
+// of the producer owns tile row q (q < RT*d <= 32): it loads that row of
+// every tile, and once the consumers have finished a tile it stores the row
+// back (its own bulk group) and reuses the slot for the tile `stages` ahead.
+//   full[st]     : TMA bytes of the tile in stage st have landed
+//   computed[st] : the consumers are done with the tile in stage st
+template <int D>
+__global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTileArgs A) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int N = A.N;
+  const int rows = A.RT * D;
+  const int tile_elems = rows * N;
+  const uint32_t tile_bytes = (uint32_t)tile_elems * 16u;
+  double2 *tiles = reinterpret_cast<double2 *>(smraw);
+  double2 *Ls = tiles + (size_t)A.stages * tile_elems;
+  double2 *Rs = Ls + D * D;
+  uint64_t *full = reinterpret_cast<uint64_t *>(Rs + D * D);
+  uint64_t *computed = full + A.stages;
+  int *rid_buf = reinterpret_cast<int *>(computed + A.stages);  // 2 x kMaxTileRows
+  const int tid = threadIdx.x;
+  const bool has_r = A.rsrc != nullptr;
+
+  const int nact = *A.n_active;
+  const long long total = (long long)nact * A.tiles_per_start;
+  const long long chunk = (total + gridDim.x - 1) / gridDim.x;
+  const long long t0 = (long long)blockIdx.x * chunk;
+  const long long t1 = t0 + chunk < total ? t0 + chunk : total;
+  const int T = t1 > t0 ? (int)(t1 - t0) : 0;
+  if (T == 0) return;
+
+  if (tid == 0) {
+    for (int s = 0; s < A.stages; s++) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&computed[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto tile_of = [&](int j, int &s, int &tt) {
+    const long long t = t0 + j;
+    const int ai = (int)(t / A.tiles_per_start);
+    tt = (int)(t - (long long)ai * A.tiles_per_start);
+    s = A.active[ai];
+  };
+
+  if (tid >= kRowThreads) {
+    // ---------------- producer warp
+    const int lane = tid - kRowThreads;
+    const uint32_t row_bytes = (uint32_t)N * 16u;
+    int myrow = 0;
+    if (lane < rows) {
+      // row of tile-row q = lane (rl = q / D, a = q % D) relative to the tile base
+      myrow = A.b.abits[lane % D];
+    }
+    for (int j = 0; j < T + A.stages; j++) {
+      const int st = j % A.stages;
+      // retire tile j - stages from this stage: store it, wait until read
+      const int jr = j - A.stages;
+      if (jr >= 0 && jr < T) {
+        ptx::mbar_wait(&computed[st], (uint32_t)((jr / A.stages) & 1));
+        int s, tt;
+        tile_of(jr, s, tt);
+        if (lane < rows) {
+          const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
+          ptx::bulk_s2g(A.ct + (long long)s * A.ct_stride + (long long)row * N,
+                        tiles + (size_t)st * tile_elems + (size_t)lane * N, row_bytes);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read<0>();
+        }
+        __syncwarp();
+      }
+      if (j < T) {
+        int s, tt;
+        tile_of(j, s, tt);
+        if (lane == 0) ptx::mbar_arrive_expect_tx(&full[st], tile_bytes);
+        __syncwarp();
+        if (lane < rows) {
+          const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
+          ptx::bulk_g2s(tiles + (size_t)st * tile_elems + (size_t)lane * N,
+                        A.ct + (long long)s * A.ct_stride + (long long)row * N, row_bytes,
+                        &full[st]);
+        }
+      }
+    }
+    if (lane < rows) ptx::bulk_wait<0>();
+    return;
+  }
+
+  // ---------------- consumer warps (256 threads, named barrier 1)
+  auto csync = [] { asm volatile("bar.sync 1, %0;" ::"n"(kRowThreads) : "memory"); };
+  int cur = -1;
+  const int NC = N / D;  // column-rests
+  for (int j = 0; j < T; j++) {
+    int s, tt;
+    tile_of(j, s, tt);
+    const int st = j % A.stages;
+    if (s != cur) {  // uniform over the consumers
+      csync();
+      if (tid < D * D) {
+        const double2 *L = A.lsrc + (long long)s * A.lstride;
+        const int i = tid / D, k = tid % D;
+        Ls[tid] = A.ldag ? cconj(L[k * D + i]) : L[tid];
+        if (has_r) {
+          const double2 *R = A.rsrc + (long long)s * A.rstride;
+          Rs[tid] = A.rdag ? cconj(R[k * D + i]) : R[tid];
+        }
+      }
+      cur = s;
+      csync();
+    }
+    int *rid = rid_buf + (j & 1) * kMaxTileRows;  // global row of each tile row
+    if (tid < rows) rid[tid] = spread_rest(A.b, tt * A.RT + tid / D) | A.b.abits[tid % D];
+    ptx::mbar_wait(&full[st], (uint32_t)((j / A.stages) & 1));
+    double2 *tile = tiles + (size_t)st * tile_elems;
+    // phase 1: left multiply, one column of one row group per item
+    for (int it = tid; it < A.RT * N; it += kRowThreads) {
+      const int rl = it / N, col = it - rl * N;
+      double2 *base = tile + (size_t)rl * D * N + col;
+      double2 x[D];
+#pragma unroll
+      for (int a = 0; a < D; a++) x[a] = base[a * N];
+#pragma unroll
+      for (int a = 0; a < D; a++) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k], acc);
+        base[a * N] = acc;
+      }
+    }
+    if (has_r) {
+      csync();
+      // phase 2: right multiply, d columns ins(b, c) of one row per item
+      for (int it = tid; it < A.RT * N; it += kRowThreads) {
+        const int rl = it / N, rem = it - rl * N;
+        const int a = rem / NC, c = rem - a * NC;
+        double2 *row = tile + (size_t)(rl * D + a) * N;
+        const int cb = spread_rest(A.b, c);
+        double2 z[D];
+#pragma unroll
+        for (int b = 0; b < D; b++) z[b] = row[cb | A.b.abits[b]];
+#pragma unroll
+        for (int b = 0; b < D; b++) {
+          double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < D; k++) acc = cfma(z[k], Rs[k * D + b], acc);
+          row[cb | A.b.abits[b]] = acc;
+        }
+      }
+    }
+    csync();
+    // fused epilogue: partial environment / trace of the next step (fixed
+    // order over the tile's rows => independent of batch and sharding)
+    if (A.nx_env) {
+      const int dd2 = A.nd * A.nd;
+      for (int o = tid; o < dd2; o += kRowThreads) {
+        const int ap = A.nab[o / A.nd], bp = A.nab[o % A.nd];
+        double2 acc = make_double2(0.0, 0.0);
+        for (int q = 0; q < rows; q++) {
+          const int i = rid[q];
+          if ((i & A.nmask) == ap) {
+            const double2 v = tile[(size_t)q * N + ((i & ~A.nmask) | bp)];
+            acc.x += v.x;
+            acc.y += v.y;
+          }
+        }
+        A.part[(long long)s * A.part_stride + (long long)tt * dd2 + o] = acc;
+      }
+    }
+    if (A.nx_trace && tid == 64) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int q = 0; q < rows; q++) {
+        const double2 v = tile[(size_t)q * N + rid[q]];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      A.tpart[(long long)s * A.tpart_stride + tt] = acc;
+    }
+    // hand the tile to the producer (generic -> async proxy)
+    ptx::fence_proxy_async_smem();
+    csync();
+    if (tid == 0) ptx::mbar_arrive(&computed[st]);
+  }
+}
+
+// vstore <- identity for every (start, VARIABLE gate, direction) slot
+__global__ void k_vstore_identity(double2 *vstore, long long vstride, int S, const int2 *slots,
+                                  int nslots) {
+  const long long total = (long long)S * nslots;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long s = e / nslots;
+    const int2 sl = slots[e % nslots];  // (offset, d)
+    double2 *v = vstore + s * vstride + sl.x;
+    for (int i = 0; i < sl.y * sl.y; i++)
+      v[i] = make_double2(i / sl.y == i % sl.y ? 1.0 : 0.0, 0.0);
+  }
 }
 
 }  // namespace qf
