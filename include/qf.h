@@ -117,6 +117,9 @@ typedef struct {
   double env_bytes;         /* k_env_polar launches                        */
   int64_t sandwich_launches, env_launches;
   double sandwich_ms, env_ms; /* CUDA-event sums (profile = 1 only)        */
+  double resident_ms;       /* k_resident CUDA-event time (profile = 1)    */
+  double sweep_flops;       /* algorithmic flops of all gate applications: */
+                            /* 16 d N^2 per step, 8 d N^2 per init pass    */
 } qf_stats;
 
 void qf_params_default(qf_params *p);

@@ -85,6 +85,8 @@ class qf_stats(ctypes.Structure):
         ("env_launches", ctypes.c_int64),
         ("sandwich_ms", ctypes.c_double),
         ("env_ms", ctypes.c_double),
+        ("resident_ms", ctypes.c_double),
+        ("sweep_flops", ctypes.c_double),
     ]
 
 

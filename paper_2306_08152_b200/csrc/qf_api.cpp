@@ -65,8 +65,11 @@ qf_status check_params(const qf_circuit_s *c, const qf_params *p) {
   if (!(p->diff_tol_a >= 0.0) || !(p->diff_tol_r >= 0.0) || !(p->long_diff_r >= 0.0))
     return fail(QF_E_ARG, "diff_tol_a, diff_tol_r and long_diff_r must be >= 0");
   if (!(p->beta >= 0.0 && p->beta <= 1.0)) return fail(QF_E_ARG, "beta must lie in [0, 1]");
-  if (p->engine != QF_ENGINE_AUTO && p->engine != QF_ENGINE_STREAM)
-    return fail(QF_E_ARG, "engine not available in this build (AUTO or STREAM)");
+  if (p->engine != QF_ENGINE_AUTO && p->engine != QF_ENGINE_STREAM &&
+      p->engine != QF_ENGINE_RESIDENT)
+    return fail(QF_E_ARG, "engine must be QF_ENGINE_AUTO, _STREAM or _RESIDENT");
+  if (p->engine == QF_ENGINE_RESIDENT && c->n > 6)
+    return fail(QF_E_ARG, "the resident engine holds the tensor in shared memory: n <= 6");
   if (p->record_sweeps < 0 || p->record_count < 0)
     return fail(QF_E_ARG, "record_sweeps and record_count must be >= 0");
   if (p->record_count > 0 && p->record_sweeps > 0) {

@@ -21,6 +21,7 @@
 
 #include "qf_internal.h"
 #include "qf_kernels.cuh"
+#include "qf_resident.cuh"
 
 namespace qf {
 
@@ -28,6 +29,12 @@ namespace {
 
 constexpr int kRingMin = 2;
 constexpr int kRowsMaxQubits = 9;
+constexpr int kResidentMaxQubits = 6;
+
+int resident_threads(int n) {
+  const int items = (1 << (2 * n)) / 4;  // phase items at d = 2
+  return std::max(32, std::min(256, items));
+}
 
 // CUDA-event timing of individual launches (qf_params.profile = 1): a ring of
 // event pairs, harvested when a slot is reused and at the end of the call.
@@ -37,7 +44,7 @@ struct Profiler {
   cudaEvent_t beg[kRing] = {}, end[kRing] = {};
   int kind[kRing] = {};
   int next = 0, used = 0;
-  double ms[2] = {0.0, 0.0};
+  double ms[3] = {0.0, 0.0, 0.0};
   void init() {
     for (int i = 0; i < kRing; i++) {
       cudaEventCreate(&beg[i]);
@@ -208,7 +215,7 @@ std::pair<int, int> row_tiles(int n, int m) {
 struct Layout {
   size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
       rec_slot, rec_starts, rec_cost, rec_gates, summary, best, part, tpart, vstore, vslots,
-      total;
+      gdesc, total;
   long long vstride;  // complex per start in vstore (sum over VARIABLE gates of 2 d^2)
   int nvslots;
   int ring;
@@ -258,6 +265,7 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
     }
   L.vstore = take(std::max<size_t>(1, S * (size_t)L.vstride) * 16);
   L.vslots = take((size_t)std::max(1, L.nvslots) * 8);
+  L.gdesc = take((size_t)std::max(1, c.p) * sizeof(GateDesc));
   L.total = o;
   return L;
 }
@@ -755,11 +763,9 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     return QF_E_NOT_UNITARY;
   }
 
-  // ---- a2: InitCircuitTensor
-  E.ctx = 0;
-  QF_CHECK(E.init_ct());
-
-  // ---- a3..a7: sweeps until every start has a verdict
+  const bool resident = p.engine == QF_ENGINE_RESIDENT ||
+                        (p.engine == QF_ENGINE_AUTO && c.n <= kResidentMaxQubits);
+  int last = 0;  // last sweep enqueued (streaming engine)
   cudaEvent_t ev[2];
   QF_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   QF_CHECK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
@@ -770,7 +776,75 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       cudaEventDestroy(e[1]);
     }
   } events{ev};
-  int last = 0;  // last sweep enqueued
+  if (resident) {
+    // ---- a2..a7 in one kernel: one CTA per start, tensor in shared memory
+    std::vector<GateDesc> gd(c.p);
+    for (int k = 0; k < c.p; k++) {
+      const Bits b = make_bits(c, k);
+      GateDesc &g = gd[k];
+      g.m = b.m;
+      g.d = b.d;
+      g.kind = c.kind[k] == QF_GATE_VARIABLE ? 0 : 1;
+      g.goff = g.kind == 0 ? c.var_off[k] / 2 : c.const_off[k] / 2;
+      g.mask = b.abits[b.d - 1];
+      g.voff = E.warm && g.kind == 0 ? E.voff[k] : 0;
+      for (int a = 0; a < 8; a++) g.abits[a] = a < b.d ? b.abits[a] : 0;
+      for (int q = 0; q < kMaxQubits; q++) g.rest_pos[q] = q < c.n - b.m ? b.rest_pos[q] : 0;
+    }
+    QF_CHECK(cudaMemcpyAsync(W + E.L.gdesc, gd.data(), gd.size() * sizeof(GateDesc),
+                             cudaMemcpyHostToDevice, st));
+    h2d += (long long)(gd.size() * sizeof(GateDesc));
+    int *counter = E.n_active() + 2;
+    QF_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    ResidentArgs A{};
+    A.n = c.n;
+    A.N = N;
+    A.p = c.p;
+    A.S = S;
+    A.gd = reinterpret_cast<const GateDesc *>(W + E.L.gdesc);
+    A.vdag = E.vdag();
+    A.cmats = E.cmats();
+    A.gates = reinterpret_cast<double2 *>(E.gates());
+    A.gstride = c.var_doubles / 2;
+    A.vstore = E.warm ? reinterpret_cast<double2 *>(W + E.L.vstore) : nullptr;
+    A.vstride = E.L.vstride;
+    A.counter = counter;
+    A.dist_tol = p.dist_tol;
+    A.diff_tol_a = p.diff_tol_a;
+    A.diff_tol_r = p.diff_tol_r;
+    A.long_diff_r = p.long_diff_r;
+    A.beta = p.beta;
+    A.long_diff_count = p.long_diff_count;
+    A.min_iters = p.min_iters;
+    A.max_iters = p.max_iters;
+    A.reset_iters = p.reset_iters;
+    A.ring = E.L.ring;
+    A.hist = reinterpret_cast<double *>(W + E.L.hist);
+    A.delta = reinterpret_cast<double *>(W + E.L.delta);
+    A.iters = reinterpret_cast<int *>(W + E.L.iters);
+    A.verdict = reinterpret_cast<int *>(W + E.L.verdict);
+    A.rec_slot = rec_slot;
+    A.R = (p.record_count > 0) ? p.record_sweeps : 0;
+    A.rec_cost = reinterpret_cast<double *>(W + E.L.rec_cost);
+    A.rec_gates = reinterpret_cast<double *>(W + E.L.rec_gates);
+    A.var_doubles = c.var_doubles;
+    const int threads = resident_threads(c.n);
+    const size_t smem = (size_t)N * N * 16 + 6 * 64 * 16;
+    QF_CHECK(cudaFuncSetAttribute(k_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident, threads, smem));
+    const int g = std::max(1, std::min(S, std::max(1, per_sm) * E.nsm));
+    const int slot = E.prof.on ? E.prof.open(2, st) : -1;
+    k_resident<<<g, threads, smem, st>>>(A);
+    if (slot >= 0) E.prof.close(slot, st);
+    E.launches++;
+    QF_CHECK(cudaGetLastError());
+  } else {
+  // ---- a2: InitCircuitTensor
+  E.ctx = 0;
+  QF_CHECK(E.init_ct());
+
+  // ---- a3..a7: sweeps until every start has a verdict
   if (p.max_iters == 0) {
     QF_CHECK(E.trace(0));
   } else {
@@ -793,6 +867,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       if (it == p.max_iters) break;
     }
   }
+  }  // streaming engine
 
   // ---- a8: summaries and best start
   qf_summary *summ = out.d_summary_out ? out.d_summary_out
@@ -875,7 +950,21 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     r.stats.env_ms = E.prof.ms[1];
     r.stats.kernel_launches = E.launches;
     r.stats.sweeps = mx;
-    r.stats.engine = QF_ENGINE_STREAM;
+    r.stats.engine = resident ? QF_ENGINE_RESIDENT : QF_ENGINE_STREAM;
+    r.stats.resident_ms = E.prof.ms[2];
+    {
+      double step_f = 0.0, init_f = 0.0;
+      for (int k = 0; k < c.p; k++) {
+        step_f += 16.0 * (1 << c.arity[k]) * (double)N * N;
+        init_f += 8.0 * (1 << c.arity[k]) * (double)N * N;
+      }
+      double f = 0.0;
+      for (const auto &q : r.summary) {
+        const int inits = q.iters >= 1 ? 1 + (q.iters - 1) / p.reset_iters : 1;
+        f += q.iters * step_f + inits * init_f;
+      }
+      r.stats.sweep_flops = f;
+    }
     r.stats.start_sweeps = ss;
     r.stats.h2d_bytes += h2d;
     r.stats.d2h_bytes += d2h;

@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
       Am[o] = acc;
     }
     __syncwarp();
-    double2 *vs = A.vstore ? A.vstore + (long long)s * A.vstride + A.voff : nullptr;
+    double2 *vs = (A.vstore && D > 2) ? A.vstore + (long long)s * A.vstride + A.voff : nullptr;
     warp_polar<D>(Am, Vm, Pm, lane, vs);
     if (vs)
       for (int e = lane; e < DD; e += 32) vs[e] = Vm[e];

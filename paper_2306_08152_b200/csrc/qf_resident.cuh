@@ -1,0 +1,324 @@
+// qf_resident.cuh -- the whole QFactor instantiation of one start inside one
+// CTA, with the circuit tensor resident in shared memory (n <= 6: at most
+// 64 KiB).  Used for the small blocks of the paper's workloads (C1..C4):
+// there the streaming engine would move 32*4^n bytes through HBM per gate
+// step and pay a kernel launch per step, while here a gate step is a few
+// shared-memory passes, FP64-bound, with no launch and no HBM traffic.
+//
+// Per start (Alg. 1):  ct <- E(u_p)..E(u_1) V^dagger (init), then
+// sweeps of 2p gate steps [env (warp 0) -> polar (warp 0) -> sandwich (all
+// threads, in place)], the cost + termination state machine after every
+// sweep, a rebuild every reset_iters sweeps, until a verdict.  CTAs take
+// starts from an atomic counter; each start's arithmetic is independent of
+// which CTA runs it, so results do not depend on batching.
+#pragma once
+
+#include "qf_kernels.cuh"
+
+namespace qf {
+
+struct GateDesc {
+  int m, d, kind, goff;   // goff: complex offset in the packed gates (VAR) or in cmats (CONST)
+  int mask;               // basis bits of the location
+  int voff;               // complex offset of the backward warm-start slot in vstore
+  int abits[8];
+  int rest_pos[kMaxQubits];
+};
+
+struct ResidentArgs {
+  int n, N, p, S;
+  const GateDesc *gd;
+  const double2 *vdag;
+  const double2 *cmats;
+  double2 *gates;
+  long long gstride;  // complex per start
+  double2 *vstore;    // nullptr: cold Jacobi
+  long long vstride;
+  int *counter;       // work-stealing start counter (zeroed before launch)
+  double dist_tol, diff_tol_a, diff_tol_r, long_diff_r, beta;
+  int long_diff_count, min_iters, max_iters, reset_iters, ring;
+  double *hist;
+  double *delta;
+  int *iters;
+  int *verdict;
+  const int *rec_slot;
+  int R;
+  double *rec_cost;
+  double *rec_gates;
+  int var_doubles;
+};
+
+__device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
+  int x = 0;
+  for (int k = 0; k < n - g.m; k++) x |= ((r >> k) & 1) << g.rest_pos[k];
+  return x;
+}
+
+// ct <- E(L) ct E(R) in place (R == nullptr: one-sided), all threads.
+template <int D>
+__device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const double2 *Ls,
+                             const double2 *Rs) {
+  const int NR = N / D;  // rests
+  const int nt = blockDim.x;
+  // phase 1: item (row-rest r, column j) mixes the D rows ins(a, r) of column j
+  for (int it = threadIdx.x; it < NR * N; it += nt) {
+    const int r = it / N, j = it - r * N;
+    const int rb = rspread(g, n, r);
+    double2 x[D];
+#pragma unroll
+    for (int a = 0; a < D; a++) x[a] = ct[(rb | g.abits[a]) * N + j];
+#pragma unroll
+    for (int a = 0; a < D; a++) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k], acc);
+      ct[(rb | g.abits[a]) * N + j] = acc;
+    }
+  }
+  if (Rs == nullptr) {
+    __syncthreads();
+    return;
+  }
+  __syncthreads();
+  // phase 2: item (row i, column-rest c) mixes the D columns ins(b, c) of row i
+  for (int it = threadIdx.x; it < N * NR; it += nt) {
+    const int i = it / NR, c = it - i * NR;
+    const int cb = rspread(g, n, c);
+    double2 *row = ct + i * N;
+    double2 z[D];
+#pragma unroll
+    for (int b = 0; b < D; b++) z[b] = row[cb | g.abits[b]];
+#pragma unroll
+    for (int b = 0; b < D; b++) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < D; k++) acc = cfma(z[k], Rs[k * D + b], acc);
+      row[cb | g.abits[b]] = acc;
+    }
+  }
+  __syncthreads();
+}
+
+// warp 0: environment of gate g from the resident tensor, the update, and the
+// sandwich operands.  Writes u_new to global memory.
+template <int D>
+__device__ void res_update(const ResidentArgs &A, const double2 *ct, const GateDesc &g,
+                           double2 *u, double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm,
+                           double2 *vs, int forward, int lane) {
+  constexpr int DD = D * D;
+  const int N = A.N, R = N / D;
+  for (int e = lane; e < DD; e += 32) Uo[e] = u[e];
+  // P[a][b] = sum_r ct[ins(a,r)][ins(b,r)], r ascending per output
+  for (int o = lane; o < DD; o += 32) {
+    const int a = o / D, b = o % D;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int r = 0; r < R; r++) {
+      const int sp = rspread(g, A.n, r);
+      const double2 v = ct[(sp | g.abits[a]) * N + (sp | g.abits[b])];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    Pm[o] = acc;
+  }
+  __syncwarp();
+  for (int o = lane; o < DD; o += 32) {
+    const int r = o / D, c = o % D;
+    double2 acc = make_double2(0.0, 0.0);
+    if (!forward) {
+#pragma unroll
+      for (int k = 0; k < D; k++) acc = cfma_cj(Pm[k * D + r], Uo[k * D + c], acc);
+    } else {
+#pragma unroll
+      for (int k = 0; k < D; k++) {
+        const double2 x = Uo[r * D + k], pv = Pm[c * D + k];
+        acc.x = fma(x.x, pv.x, acc.x);
+        acc.x = fma(x.y, pv.y, acc.x);
+        acc.y = fma(x.y, pv.x, acc.y);
+        acc.y = fma(-x.x, pv.y, acc.y);
+      }
+    }
+    if (A.beta != 0.0) {
+      acc = cscale(acc, 1.0 - A.beta);
+      acc.x = fma(A.beta, Uo[o].x, acc.x);
+      acc.y = fma(A.beta, Uo[o].y, acc.y);
+    }
+    Am[o] = acc;
+  }
+  __syncwarp();
+  warp_polar<D>(Am, Vm, Pm, lane, vs);  // u_new -> Pm
+  if (vs)
+    for (int e = lane; e < DD; e += 32) vs[e] = Vm[e];
+  for (int e = lane; e < DD; e += 32) u[e] = Pm[e];
+  __syncwarp();
+}
+
+template <int D>
+__device__ void res_step(const ResidentArgs &A, double2 *ct, const GateDesc &g, int s, int forward,
+                         double2 *Ls, double2 *Rs, double2 *Uo, double2 *Pm, double2 *Am,
+                         double2 *Vm) {
+  constexpr int DD = D * D;
+  const int tid = threadIdx.x;
+  if (g.kind == 0) {
+    double2 *u = A.gates + (long long)s * A.gstride + g.goff;
+    if (tid < 32) {
+      double2 *vs = (A.vstore && D > 2)
+                        ? A.vstore + (long long)s * A.vstride + g.voff + (forward ? DD : 0)
+                        : nullptr;
+      res_update<D>(A, ct, g, u, Uo, Pm, Am, Vm, vs, forward, tid);
+      // operands: backward L = u_old^dagger, R = u_new; forward L = u_new, R = u_old^dagger
+      for (int e = tid; e < DD; e += 32) {
+        const int i = e / D, k = e % D;
+        const double2 od = cconj(Uo[k * D + i]);
+        Ls[e] = forward ? Pm[e] : od;
+        Rs[e] = forward ? od : Pm[e];
+      }
+    }
+  } else {
+    const double2 *cm = A.cmats + g.goff;
+    for (int e = tid; e < DD; e += blockDim.x) {
+      const int i = e / D, k = e % D;
+      const double2 cd = cconj(cm[k * D + i]);
+      Ls[e] = forward ? cm[e] : cd;
+      Rs[e] = forward ? cd : cm[e];
+    }
+  }
+  __syncthreads();
+  res_sandwich<D>(ct, g, A.n, A.N, Ls, Rs);
+}
+
+template <int D>
+__device__ void res_apply_left(double2 *ct, const GateDesc &g, const ResidentArgs &A,
+                               const double2 *src, double2 *Ls) {
+  for (int e = threadIdx.x; e < D * D; e += blockDim.x) Ls[e] = src[e];
+  __syncthreads();
+  res_sandwich<D>(ct, g, A.n, A.N, Ls, nullptr);
+}
+
+__device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gdesc, int s,
+                         double2 *Ls) {
+  const int NN = A.N * A.N;
+  for (int e = threadIdx.x; e < NN; e += blockDim.x) ct[e] = A.vdag[e];
+  __syncthreads();
+  for (int k = 0; k < A.p; k++) {
+    const GateDesc &g = gdesc[k];
+    const double2 *src = g.kind == 0 ? A.gates + (long long)s * A.gstride + g.goff : A.cmats + g.goff;
+    switch (g.d) {
+      case 2: res_apply_left<2>(ct, g, A, src, Ls); break;
+      case 4: res_apply_left<4>(ct, g, A, src, Ls); break;
+      default: res_apply_left<8>(ct, g, A, src, Ls); break;
+    }
+  }
+  if (A.vstore) {  // warm starts restart from I with every (re)build
+    for (int k = 0; k < A.p; k++) {
+      const GateDesc &g = gdesc[k];
+      if (g.kind != 0) continue;
+      double2 *v = A.vstore + (long long)s * A.vstride + g.voff;
+      for (int e = threadIdx.x; e < 2 * g.d * g.d; e += blockDim.x) {
+        const int q = e % (g.d * g.d);
+        v[e] = make_double2(q / g.d == q % g.d ? 1.0 : 0.0, 0.0);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_resident(const ResidentArgs A) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double2 *ct = reinterpret_cast<double2 *>(smraw);
+  double2 *Ls = ct + A.N * A.N;
+  double2 *Rs = Ls + 64;
+  double2 *Uo = Rs + 64;
+  double2 *Pm = Uo + 64;
+  double2 *Am = Pm + 64;
+  double2 *Vm = Am + 64;
+  const GateDesc *gdesc = A.gd;  // global, read through L1
+  __shared__ int s_start, s_verdict;
+  const int tid = threadIdx.x;
+  for (;;) {
+    if (tid == 0) s_start = atomicAdd(A.counter, 1);
+    __syncthreads();
+    const int s = s_start;
+    if (s >= A.S) break;
+    res_init(A, ct, gdesc, s, Ls);
+    int it = 0;
+    for (;;) {
+      if (A.max_iters > 0) {
+        for (int k = A.p - 1; k >= 0; k--) {
+          const GateDesc &g = gdesc[k];
+          switch (g.d) {
+            case 2: res_step<2>(A, ct, g, s, 0, Ls, Rs, Uo, Pm, Am, Vm); break;
+            case 4: res_step<4>(A, ct, g, s, 0, Ls, Rs, Uo, Pm, Am, Vm); break;
+            default: res_step<8>(A, ct, g, s, 0, Ls, Rs, Uo, Pm, Am, Vm); break;
+          }
+        }
+        for (int k = 0; k < A.p; k++) {
+          const GateDesc &g = gdesc[k];
+          switch (g.d) {
+            case 2: res_step<2>(A, ct, g, s, 1, Ls, Rs, Uo, Pm, Am, Vm); break;
+            case 4: res_step<4>(A, ct, g, s, 1, Ls, Rs, Uo, Pm, Am, Vm); break;
+            default: res_step<8>(A, ct, g, s, 1, Ls, Rs, Uo, Pm, Am, Vm); break;
+          }
+        }
+        it++;
+      }
+      // cost + termination, warp 0
+      if (tid < 32) {
+        double re = 0.0, im = 0.0;
+        for (int i = tid; i < A.N; i += 32) {
+          re += ct[i * A.N + i].x;
+          im += ct[i * A.N + i].y;
+        }
+        for (int off = 1; off < 32; off <<= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, off);
+          im += __shfl_xor_sync(0xffffffffu, im, off);
+        }
+        const double c = 1.0 - hypot(re, im) / (double)A.N;
+        if (tid == 0) {
+          int v = 0;
+          if (it == 0) {
+            v = 4;
+          } else {
+            double *h = A.hist + (long long)s * A.ring;
+            h[it % A.ring] = c;
+            if (!isfinite(c)) {
+              v = 5;
+            } else {
+              if (it >= A.min_iters) {
+                const int L = A.long_diff_count;
+                if (c <= A.dist_tol) {
+                  v = 1;
+                } else if (it >= 2 &&
+                           fabs(c - h[(it - 1) % A.ring]) <= A.diff_tol_a + A.diff_tol_r * c) {
+                  v = 2;
+                } else if (L > 0 && it > L) {
+                  const double cl = h[(it - L) % A.ring];
+                  if (cl - c <= A.long_diff_r * cl) v = 3;
+                }
+              }
+              if (v == 0 && it >= A.max_iters) v = 4;
+            }
+          }
+          s_verdict = v;
+          A.delta[s] = c;
+          A.iters[s] = it;
+          A.verdict[s] = v;
+        }
+        if (A.R > 0 && it >= 1 && it <= A.R) {
+          const int slot = A.rec_slot[s];
+          if (slot >= 0) {
+            if (tid == 0) A.rec_cost[(long long)slot * A.R + it - 1] = c;
+            const double *gsrc = reinterpret_cast<const double *>(A.gates + (long long)s * A.gstride);
+            double *dst = A.rec_gates + ((long long)slot * A.R + it - 1) * A.var_doubles;
+            for (int e = tid; e < A.var_doubles; e += 32) dst[e] = gsrc[e];
+          }
+        }
+      }
+      __syncthreads();
+      if (s_verdict != 0) break;
+      if (it % A.reset_iters == 0) res_init(A, ct, gdesc, s, Ls);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace qf
