@@ -24,6 +24,7 @@ QF_GATE_VARIABLE, QF_GATE_CONSTANT = 0, 1
 QF_RUNNING, QF_CONVERGED, QF_PLATEAU_SHORT, QF_PLATEAU_LONG, QF_MAX_ITER, QF_NUMERIC_FAIL = range(6)
 QF_ENGINE_AUTO, QF_ENGINE_STREAM, QF_ENGINE_RESIDENT = range(3)
 
+ENGINE_NAMES = {0: "auto", 1: "stream", 2: "resident"}
 VERDICT_NAMES = {0: "RUNNING", 1: "CONVERGED", 2: "PLATEAU_SHORT", 3: "PLATEAU_LONG",
                  4: "MAX_ITER", 5: "NUMERIC_FAIL"}
 

@@ -32,8 +32,10 @@ constexpr int kRowsMaxQubits = 9;
 constexpr int kResidentMaxQubits = 6;
 
 int resident_threads(int n) {
-  const int items = (1 << (2 * n)) / 4;  // phase items at d = 2
-  return std::max(32, std::min(256, items));
+  // 32 (n <= 3), 64 (n = 4), 128 (n >= 5): with ~126 registers per thread,
+  // 128 threads keep 3 CTAs (= 3 resident 64 KiB tensors at n = 6) per SM
+  const int items = (1 << (2 * n)) / 4;
+  return std::max(32, std::min(128, items));
 }
 
 // CUDA-event timing of individual launches (qf_params.profile = 1): a ring of
@@ -830,12 +832,15 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.var_doubles = c.var_doubles;
     const int threads = resident_threads(c.n);
     const size_t smem = (size_t)N * N * 16 + 6 * 64 * 16;
-    QF_CHECK(cudaFuncSetAttribute(k_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int maxm = 1;
+    for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
+    auto kern = maxm == 1 ? k_resident<2> : maxm == 2 ? k_resident<4> : k_resident<8>;
+    QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resident, threads, smem));
+    QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     const int g = std::max(1, std::min(S, std::max(1, per_sm) * E.nsm));
     const int slot = E.prof.on ? E.prof.open(2, st) : -1;
-    k_resident<<<g, threads, smem, st>>>(A);
+    kern<<<g, threads, smem, st>>>(A);
     if (slot >= 0) E.prof.close(slot, st);
     E.launches++;
     QF_CHECK(cudaGetLastError());
@@ -958,12 +963,18 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
         step_f += 16.0 * (1 << c.arity[k]) * (double)N * N;
         init_f += 8.0 * (1 << c.arity[k]) * (double)N * N;
       }
-      double f = 0.0;
+      double f = 0.0, passes = 0.0;
       for (const auto &q : r.summary) {
         const int inits = q.iters >= 1 ? 1 + (q.iters - 1) / p.reset_iters : 1;
         f += q.iters * step_f + inits * init_f;
+        passes += (double)q.iters * 2 * c.p + (double)inits * c.p;
       }
       r.stats.sweep_flops = f;
+      if (resident) {  // HBM-equivalent algorithmic bytes of the on-chip passes
+        r.stats.sandwich_bytes = passes * 32.0 * N * N;
+        r.stats.alg_bytes_total = r.stats.sandwich_bytes;
+        r.stats.sandwich_launches = 0;
+      }
     }
     r.stats.start_sweeps = ss;
     r.stats.h2d_bytes += h2d;

@@ -268,6 +268,39 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
   if (v0) {
     for (int e = lane; e < D * D; e += 32) Vm[e] = v0[e];
     __syncwarp();
+    // re-unitarise the stored V with one Newton-Schulz step,
+    // V <- V (3I - V^H V) / 2, so rounding drift does not accumulate across
+    // reuses (unitarity error e -> O(e^2)); U is scratch here
+    for (int o = lane; o < D * D; o += 32) {
+      const int r = o / D, c = o % D;
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < D; k++) acc = cfma_cj(Vm[k * D + r], Vm[k * D + c], acc);
+      U[o] = acc;  // (V^H V)[r][c]
+    }
+    __syncwarp();
+    double2 nv[(D * D + 31) / 32];
+#pragma unroll
+    for (int q = 0; q < (D * D + 31) / 32; q++) {
+      const int o = lane + 32 * q;
+      nv[q] = make_double2(0.0, 0.0);
+      if (o < D * D) {
+        const int r = o / D, c = o % D;
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < D; k++) {
+          const double2 w = U[k * D + c];
+          const double2 t = make_double2((k == c ? 1.5 : 0.0) - 0.5 * w.x, -0.5 * w.y);
+          acc = cfma(Vm[r * D + k], t, acc);
+        }
+        nv[q] = acc;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < (D * D + 31) / 32; q++)
+      if (lane + 32 * q < D * D) Vm[lane + 32 * q] = nv[q];
+    __syncwarp();
     for (int o = lane; o < D * D; o += 32) {
       const int r = o / D, c = o % D;
       double2 acc = make_double2(0.0, 0.0);
@@ -308,15 +341,21 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
         ga.x += __shfl_xor_sync(0xffffffffu, ga.x, off);
         ga.y += __shfl_xor_sync(0xffffffffu, ga.y, off);
       }
-      const double g = sqrt(cabs2(ga));
-      const bool rot = act && g > 0.0 && g > 1e-15 * sqrt(al * be);
+      const double g2 = cabs2(ga);
+      // rotate iff |gamma| > 1e-15 sqrt(alpha beta)  (squared: no sqrt)
+      const bool rot = act && g2 > 0.0 && g2 > 1e-30 * (al * be);
       if (rot) {
         // e^{-i phi} = conj(gamma)/|gamma| makes the 2x2 Gram real; then the
-        // symmetric Schur rotation (Golub & Van Loan 8.4.1).
-        const double2 ph = make_double2(ga.x / g, -ga.y / g);
-        const double zeta = (be - al) / (2.0 * g);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        // symmetric Schur rotation (Golub & Van Loan 8.4.1) with
+        // zeta = y / (2g), y = beta - alpha, written without the divisions:
+        // t = sign(y) 2g / (|y| + sqrt(4 g^2 + y^2)), c = 1/sqrt(1+t^2).
+        const double inv_g = rsqrt(g2);
+        const double g = g2 * inv_g;
+        const double y = be - al;
+        const double r = sqrt(fma(4.0, g2, y * y));
+        const double t = (y >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(y) + r);
+        const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+        const double2 ph = make_double2(ga.x * inv_g, -ga.y * inv_g);
         const double2 aq2 = cmul(aq, ph), vq2 = cmul(vq, ph);
         Am[i * D + cp] = make_double2(c * ap.x - s * aq2.x, c * ap.y - s * aq2.y);
         Am[i * D + cq] = make_double2(s * ap.x + c * aq2.x, s * ap.y + c * aq2.y);

@@ -54,6 +54,45 @@ __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
   return x;
 }
 
+// ct <- E(L) ct E(R) in place for D <= 4, one D x D block (row-rest r,
+// column-rest c) per item held in registers: one shared-memory read and write
+// per element and a single barrier per step.
+template <int D>
+__device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N,
+                                    const double2 *Ls, const double2 *Rs) {
+  const int NR = N / D;
+  for (int it = threadIdx.x; it < NR * NR; it += blockDim.x) {
+    const int r = it / NR, c = it - r * NR;
+    const int rb = rspread(g, n, r), cb = rspread(g, n, c);
+    double2 x[D][D];
+#pragma unroll
+    for (int a = 0; a < D; a++)
+#pragma unroll
+      for (int b = 0; b < D; b++) x[a][b] = ct[(rb | g.abits[a]) * N + (cb | g.abits[b])];
+    // row by row: z[a][:] = (L[a][:] x) R, stored over the (register-held) block
+#pragma unroll
+    for (int a = 0; a < D; a++) {
+      double2 y[D];
+#pragma unroll
+      for (int b = 0; b < D; b++) y[b] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < D; k++) {
+        const double2 l = Ls[a * D + k];
+#pragma unroll
+        for (int b = 0; b < D; b++) y[b] = cfma(l, x[k][b], y[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < D; b++) {
+        double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < D; k++) z = cfma(y[k], Rs[k * D + b], z);
+        ct[(rb | g.abits[a]) * N + (cb | g.abits[b])] = z;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // ct <- E(L) ct E(R) in place (R == nullptr: one-sided), all threads.
 template <int D>
 __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const double2 *Ls,
@@ -183,7 +222,26 @@ __device__ void res_step(const ResidentArgs &A, double2 *ct, const GateDesc &g, 
     }
   }
   __syncthreads();
-  res_sandwich<D>(ct, g, A.n, A.N, Ls, Rs);
+  if constexpr (D <= 4)
+    res_sandwich_blocks<D>(ct, g, A.n, A.N, Ls, Rs);
+  else
+    res_sandwich<D>(ct, g, A.n, A.N, Ls, Rs);
+}
+
+// one gate step dispatched on the gate's arity (only arities <= MAXD exist)
+template <int MAXD>
+__device__ __forceinline__ void res_step_any(const ResidentArgs &A, double2 *ct, const GateDesc &g,
+                                             int s, int forward, double2 *Ls, double2 *Rs,
+                                             double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm) {
+  if (g.d == 2) {
+    res_step<2>(A, ct, g, s, forward, Ls, Rs, Uo, Pm, Am, Vm);
+  } else if constexpr (MAXD >= 4) {
+    if (g.d == 4) {
+      res_step<4>(A, ct, g, s, forward, Ls, Rs, Uo, Pm, Am, Vm);
+    } else if constexpr (MAXD >= 8) {
+      res_step<8>(A, ct, g, s, forward, Ls, Rs, Uo, Pm, Am, Vm);
+    }
+  }
 }
 
 template <int D>
@@ -194,6 +252,7 @@ __device__ void res_apply_left(double2 *ct, const GateDesc &g, const ResidentArg
   res_sandwich<D>(ct, g, A.n, A.N, Ls, nullptr);
 }
 
+template <int MAXD>
 __device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gdesc, int s,
                          double2 *Ls) {
   const int NN = A.N * A.N;
@@ -202,10 +261,14 @@ __device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gde
   for (int k = 0; k < A.p; k++) {
     const GateDesc &g = gdesc[k];
     const double2 *src = g.kind == 0 ? A.gates + (long long)s * A.gstride + g.goff : A.cmats + g.goff;
-    switch (g.d) {
-      case 2: res_apply_left<2>(ct, g, A, src, Ls); break;
-      case 4: res_apply_left<4>(ct, g, A, src, Ls); break;
-      default: res_apply_left<8>(ct, g, A, src, Ls); break;
+    if (g.d == 2) {
+      res_apply_left<2>(ct, g, A, src, Ls);
+    } else if constexpr (MAXD >= 4) {
+      if (g.d == 4) {
+        res_apply_left<4>(ct, g, A, src, Ls);
+      } else if constexpr (MAXD >= 8) {
+        res_apply_left<8>(ct, g, A, src, Ls);
+      }
     }
   }
   if (A.vstore) {  // warm starts restart from I with every (re)build
@@ -222,7 +285,8 @@ __device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gde
   }
 }
 
-__global__ void __launch_bounds__(256) k_resident(const ResidentArgs A) {
+template <int MAXD>
+__global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   double2 *ct = reinterpret_cast<double2 *>(smraw);
   double2 *Ls = ct + A.N * A.N;
@@ -239,26 +303,14 @@ __global__ void __launch_bounds__(256) k_resident(const ResidentArgs A) {
     __syncthreads();
     const int s = s_start;
     if (s >= A.S) break;
-    res_init(A, ct, gdesc, s, Ls);
+    res_init<MAXD>(A, ct, gdesc, s, Ls);
     int it = 0;
     for (;;) {
       if (A.max_iters > 0) {
-        for (int k = A.p - 1; k >= 0; k--) {
-          const GateDesc &g = gdesc[k];
-          switch (g.d) {
-            case 2: res_step<2>(A, ct, g, s, 0, Ls, Rs, Uo, Pm, Am, Vm); break;
-            case 4: res_step<4>(A, ct, g, s, 0, Ls, Rs, Uo, Pm, Am, Vm); break;
-            default: res_step<8>(A, ct, g, s, 0, Ls, Rs, Uo, Pm, Am, Vm); break;
-          }
-        }
-        for (int k = 0; k < A.p; k++) {
-          const GateDesc &g = gdesc[k];
-          switch (g.d) {
-            case 2: res_step<2>(A, ct, g, s, 1, Ls, Rs, Uo, Pm, Am, Vm); break;
-            case 4: res_step<4>(A, ct, g, s, 1, Ls, Rs, Uo, Pm, Am, Vm); break;
-            default: res_step<8>(A, ct, g, s, 1, Ls, Rs, Uo, Pm, Am, Vm); break;
-          }
-        }
+        for (int k = A.p - 1; k >= 0; k--)
+          res_step_any<MAXD>(A, ct, gdesc[k], s, 0, Ls, Rs, Uo, Pm, Am, Vm);
+        for (int k = 0; k < A.p; k++)
+          res_step_any<MAXD>(A, ct, gdesc[k], s, 1, Ls, Rs, Uo, Pm, Am, Vm);
         it++;
       }
       // cost + termination, warp 0
@@ -315,7 +367,7 @@ __global__ void __launch_bounds__(256) k_resident(const ResidentArgs A) {
       }
       __syncthreads();
       if (s_verdict != 0) break;
-      if (it % A.reset_iters == 0) res_init(A, ct, gdesc, s, Ls);
+      if (it % A.reset_iters == 0) res_init<MAXD>(A, ct, gdesc, s, Ls);
     }
     __syncthreads();
   }

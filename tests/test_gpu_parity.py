@@ -93,60 +93,93 @@ def _compare(gpu, orc_P, idx, R, N, check_final=True):
     return borderline
 
 
-def _run_pair(n, locs, kinds, cm, V, initial, R=10, sample=None, **params):
+def _run_pair(n, locs, kinds, cm, V, initial, R=10, sample=None, engine=qf.QF_ENGINE_AUTO,
+              **params):
     c = qf.Circuit(n, locs, kinds, cm)
     S = initial.shape[0]
     idx = np.arange(S) if sample is None else np.asarray(sample)
-    gpu = qf.qf_instantiate(c, V, initial, record_starts=idx, record_sweeps=R, **params)
+    gpu = qf.qf_instantiate(c, V, initial, record_starts=idx, record_sweeps=R, engine=engine,
+                            **params)
+    exp = engine if engine != qf.QF_ENGINE_AUTO else (
+        qf.QF_ENGINE_RESIDENT if n <= 6 else qf.QF_ENGINE_STREAM)
+    assert gpu.stats["engine"] == exp
     orc = _oracle(n, locs, kinds, cm, V, initial[idx], R, **params)
     return gpu, orc, idx
 
 
-@pytest.mark.parametrize("n,p,seed", [(1, 4, 0), (2, 7, 1), (3, 9, 2), (4, 10, 3), (5, 8, 4),
-                                      (6, 9, 5), (7, 7, 6), (8, 6, 7)])
-def test_parity_random_templates(n, p, seed):
+ENGINES = [qf.QF_ENGINE_STREAM, qf.QF_ENGINE_RESIDENT]
+RANDOM = [(1, 4, 0), (2, 7, 1), (3, 9, 2), (4, 10, 3), (5, 8, 4), (6, 9, 5), (7, 7, 6), (8, 6, 7),
+          (9, 4, 8)]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("n,p,seed", RANDOM)
+def test_parity_random_templates(n, p, seed, engine):
     """Random arities 1-3, random (unsorted) locations, 25% CONSTANT gates,
-    a ragged 37 starts, Haar target, 10 recorded sweeps."""
+    a ragged 37 starts, Haar target, 10 recorded sweeps; both engines."""
+    if engine == qf.QF_ENGINE_RESIDENT and n > 6:
+        pytest.skip("resident engine: n <= 6")
     locs, kinds, cm = qfgen.random_template(n, p, seed=seed, const_frac=0.25)
     V = qfgen.haar(qfgen.stream_key(seed, qfgen.PURPOSE_TARGET, 0, 0), 2 ** n)[0]
-    init = qfgen.initial_gates(n, locs, kinds, 3000 + seed, 0, 37)
-    gpu, orc, idx = _run_pair(n, locs, kinds, cm, V, init, R=10, max_iters=10)
+    S = 37 if n <= 8 else 5
+    init = qfgen.initial_gates(n, locs, kinds, 3000 + seed, 0, S)
+    gpu, orc, idx = _run_pair(n, locs, kinds, cm, V, init, R=10, max_iters=10 if n <= 8 else 3,
+                              engine=engine)
     _compare(gpu, orc, idx, 10, 2 ** n)
 
 
+def test_parity_n10_tile_kernel():
+    """n = 10 takes the register-tile sandwich (rows of 16 KiB are beyond the
+    row-tile kernel); 2 starts x 2 sweeps."""
+    n = 10
+    locs, kinds, cm = qfgen.random_template(n, 3, arities=(2, 3), seed=21)
+    V = qfgen.haar(qfgen.stream_key(21, qfgen.PURPOSE_TARGET, 0, 0), 2 ** n)[0]
+    init = qfgen.initial_gates(n, locs, kinds, 3021, 0, 2)
+    gpu, orc, idx = _run_pair(n, locs, kinds, cm, V, init, R=2, max_iters=2)
+    _compare(gpu, orc, idx, 2, 2 ** n)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("name", ["C1", "C2+"])
-def test_parity_full_run(name):
+def test_parity_full_run(name, engine):
     w = qfgen.workload(name)
     gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(),
-                              w.initial(), R=10, max_iters=w.max_iters)
+                              w.initial(), R=10, max_iters=w.max_iters, engine=engine)
     _compare(gpu, orc, idx, 10, 2 ** w.n)
     if name == "C1":  # KAK universality: converged starts reach dist_tol
         assert (gpu.verdict == qf.QF_CONVERGED).sum() >= 1
 
 
-def test_parity_C2_full():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_parity_C2_full(engine):
     w = qfgen.workload("C2")
     gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(),
-                              w.initial(), R=10, max_iters=w.max_iters)
+                              w.initial(), R=10, max_iters=w.max_iters, engine=engine)
     _compare(gpu, orc, idx, 10, 2 ** w.n)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("name,sample", [("C3", [0, 1, 2, 511, 1022, 1023]),
                                          ("C3+", [0, 5, 700, 1023])])
-def test_parity_C3_sampled(name, sample):
+def test_parity_C3_sampled(name, sample, engine):
     w = qfgen.workload(name)
     gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(),
-                              w.initial(), R=10, sample=sample, max_iters=w.max_iters)
+                              w.initial(), R=10, sample=sample, max_iters=w.max_iters,
+                              engine=engine)
     _compare(gpu, orc, idx, 10, 2 ** w.n)
 
 
-def test_parity_C4_bench_config():
-    """The bench workload at full size (4096 starts): every start runs to its
-    verdict on the GPU; sampled starts are re-run to verdict by the oracle."""
+@pytest.mark.parametrize("engine", [qf.QF_ENGINE_AUTO, qf.QF_ENGINE_STREAM])
+def test_parity_C4_bench_config(engine):
+    """The bench workload at full size (4096 starts) in the launch
+    configuration bench.py times (AUTO = resident engine), and on the
+    streaming engine: every start runs to its verdict on the GPU; sampled
+    starts are re-run to verdict by the oracle."""
     w = qfgen.workload("C4")
     sample = [0, 1, 2047, 4094, 4095]
     gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(),
-                              w.initial(), R=10, sample=sample, max_iters=w.max_iters)
+                              w.initial(), R=10, sample=sample, max_iters=w.max_iters,
+                              engine=engine)
     _compare(gpu, orc, idx, 10, 2 ** w.n)
     assert np.all(gpu.verdict != qf.QF_RUNNING)
     assert np.all(gpu.delta <= 1.0) and np.all(gpu.delta >= -1e-14)
@@ -185,12 +218,13 @@ def test_constant_only_circuit():
     _compare(gpu, orc, idx, 3, 2 ** 3)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("kw", [{"beta": 0.5}, {"reset_iters": 1}, {"min_iters": 7},
                                 {"diff_tol_a": 1e-3}, {"long_diff_count": 0}])
-def test_parity_hyperparameters(kw):
+def test_parity_hyperparameters(kw, engine):
     w = qfgen.workload("C3+")
     gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(),
-                              w.initial(0, 24), R=10, max_iters=60, **kw)
+                              w.initial(0, 24), R=10, max_iters=60, engine=engine, **kw)
     _compare(gpu, orc, idx, 10, 2 ** w.n)
 
 
@@ -218,19 +252,20 @@ def test_rejects_non_unitary_inputs():
 
 
 # ------------------------------------------------------------------ invariance
-def test_sharding_invariance_bitwise():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_sharding_invariance_bitwise(engine):
     """Per-start results do not depend on batch composition (fixed-order
     reductions only): 100 starts at once == two shards of 50."""
     w = qfgen.workload("C3")
     c = qf.Circuit.from_workload(w)
     V = w.target_unitary()
-    a = qf.qf_instantiate(c, V, w.initial(0, 100), max_iters=300)
-    b1 = qf.qf_instantiate(c, V, w.initial(0, 50), max_iters=300)
-    b2 = qf.qf_instantiate(c, V, w.initial(50, 50), max_iters=300)
+    a = qf.qf_instantiate(c, V, w.initial(0, 100), max_iters=300, engine=engine)
+    b1 = qf.qf_instantiate(c, V, w.initial(0, 50), max_iters=300, engine=engine)
+    b2 = qf.qf_instantiate(c, V, w.initial(50, 50), max_iters=300, engine=engine)
     for f in ("delta", "iters", "verdict"):
         assert np.array_equal(a.summary[f], np.concatenate([b1.summary[f], b2.summary[f]]))
     assert np.array_equal(a.gates, np.concatenate([b1.gates, b2.gates]))
-    a2 = qf.qf_instantiate(c, V, w.initial(0, 100), max_iters=300)
+    a2 = qf.qf_instantiate(c, V, w.initial(0, 100), max_iters=300, engine=engine)
     assert np.array_equal(a.summary, a2.summary) and np.array_equal(a.gates, a2.gates)
 
 

@@ -435,3 +435,17 @@ def test_default_params_golden(orc):
     for k in ("dist_tol", "diff_tol_a", "diff_tol_r", "long_diff_count", "long_diff_r",
               "min_iters", "max_iters", "reset_iters", "beta"):
         assert getattr(P, k) == g[k], k
+
+
+def test_oracle_regression_C1_golden(orc):
+    """Regression fixture written by tests/golden/make_golden.py (oracle only)."""
+    g = json.load(open(os.path.join(GOLD, "oracle_C1_trajectories.json")))
+    w = qfgen.workload("C1")
+    r = orc.instantiate(orc.Circuit(w.n, w.locs, w.kinds, w.const_mats), w.target_unitary(),
+                        w.initial(), orc.default_params(max_iters=w.max_iters), record_sweeps=30,
+                        nthreads=1)
+    assert r.verdict.tolist() == g["verdict"] and r.iters.tolist() == g["iters"]
+    assert np.abs(r.delta - np.array(g["delta"])).max() < 1e-13
+    ref = np.array([[np.nan if x is None else x for x in row] for row in g["cost_first30"]])
+    assert np.array_equal(np.isnan(ref), np.isnan(r.cost_hist))
+    assert np.nanmax(np.abs(ref - r.cost_hist)) < 1e-13

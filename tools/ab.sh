@@ -1,14 +1,18 @@
 #!/bin/bash
-# A/B timings of kernel variants on C4 (3 sweeps) and C5 (1 sweep)
+# A/B timings of kernel variants: C4 (3 sweeps), C5 (1 sweep); resident vs stream on C4/C3
 run() { python tools/profile_case.py $1 $2 2 | python -c "
 import sys,ast
 for line in sys.stdin:
     name,_,it,_,st=line.split(' ',4)
     s=ast.literal_eval(st.strip())
-    print(name,'sandwich GB/s',round(s['sandwich_bytes']/1e9/(s['sandwich_ms']/1e3)),'avg us',round(1e3*s['sandwich_ms']/s['sandwich_launches'],1),'env avg us',round(1e3*s['env_ms']/max(1,s['env_launches']),1), 'alg GB', round(s['alg_bytes_total']/1e9,1))
+    ms = s['resident_ms'] if s['engine']==2 else s['sandwich_ms']
+    print(name,'engine',s['engine'],'sandwich/resident ms',round(ms,2),'GB/s',round(s['sandwich_bytes']/1e9/(s['sandwich_ms']/1e3)) if s['sandwich_ms'] else '-','avg us',round(1e3*s['sandwich_ms']/max(1,s['sandwich_launches']),1),'env avg us',round(1e3*s['env_ms']/max(1,s['env_launches']),1), 'GFLOP/s', round(s['sweep_flops']/1e9/(ms/1e3)) if ms else '-')
 "; }
 for cfg in "C4 3" "C5 1"; do
-  echo "== $cfg rows+warm";   run $cfg
-  echo "== $cfg rows cold";   QF_WARM=0 run $cfg
-  echo "== $cfg tile";   QF_SANDWICH=tile run $cfg
+  echo "== $cfg stream rows";   QF_ENGINE=stream run $cfg
+  echo "== $cfg stream tile";   QF_ENGINE=stream QF_SANDWICH=tile run $cfg
+done
+for cfg in "C4 3" "C3 20" "C2 50"; do
+  echo "== $cfg resident";   QF_ENGINE=resident run $cfg
+  echo "== $cfg stream";   QF_ENGINE=stream run $cfg
 done

@@ -20,7 +20,9 @@ c = qf.Circuit.from_workload(w)
 dV = torch.from_numpy(np.ascontiguousarray(w.target_unitary())).to(dev)
 dI = torch.from_numpy(w.initial()).to(dev)
 ws = torch.empty(qf.qf_workspace_size(c, w.starts, max_iters=iters), dtype=torch.uint8, device=dev)
+eng = {"stream": qf.QF_ENGINE_STREAM, "resident": qf.QF_ENGINE_RESIDENT}.get(
+    os.environ.get("QF_ENGINE", "auto"), qf.QF_ENGINE_AUTO)
 for _ in range(reps):
-    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=iters, profile=1)
+    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=iters, profile=1, engine=eng)
 torch.cuda.synchronize()
 print(name, "iters", iters, "stats", r.stats)
