@@ -335,7 +335,9 @@ struct Engine {
   char *ws;
   Layout L;
   int S, N, nsm = 148;
-  bool use_rows = true;  // QF_SANDWICH=tile forces the register-tile kernel (A/B runs)
+  // sandwich kernel choice: 0 auto (d <= 4: register blocks; d = 8: TMA row
+  // tiles up to n = 9, else smem tiles); QF_SANDWICH=rows|tile|reg forces one
+  int sw_kind = 0;
   bool warm = true;      // QF_WARM=0 disables the warm-started Jacobi (A/B runs)
   std::vector<int> voff; // per gate: complex offset of its backward slot in vstore
   long long launches = 0;
@@ -363,7 +365,10 @@ struct Engine {
     env_ctx.assign((size_t)p.max_iters + 2, 0);
     env_bytes_ctx.assign((size_t)p.max_iters + 2, 0);
     if (p.profile) prof.init();
-    if (const char *e = getenv("QF_SANDWICH")) use_rows = std::string(e) != "tile";
+    if (const char *e = getenv("QF_SANDWICH")) {
+      const std::string v(e);
+      sw_kind = v == "rows" ? 1 : v == "tile" ? 2 : v == "reg" ? 3 : 0;
+    }
     if (const char *e = getenv("QF_WARM")) warm = std::string(e) != "0";
     voff.assign(c.p, -1);
     long long o = 0;
@@ -464,8 +469,34 @@ struct Engine {
   // fused partials available for env(part_k, part_dir) / the trace
   int part_k = -1, part_dir = 0, part_tiles = 0, tpart_tiles = 0;
 
+  template <int D>
+  cudaError_t launch_reg(const SandwichArgs &A) {
+    int &grid = reg_grid[ilog2(D)];
+    if (grid == 0) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sandwich_reg<D>, 256, 0);
+      grid = std::max(1, per_sm) * nsm;
+    }
+    const int NR = N / D;
+    const long long total = (long long)S * ((NR * NR + 255) / 256);
+    const int g = (int)std::max<long long>(1, std::min<long long>(grid, total));
+    const int slot = prof.on ? prof.open(0, st) : -1;
+    k_sandwich_reg<D><<<g, 256, 0, st>>>(A);
+    if (slot >= 0) prof.close(slot, st);
+    launches++;
+    sw_ctx[ctx]++;
+    return cudaGetLastError();
+  }
+  int reg_grid[4] = {0, 0, 0, 0};
+
   cudaError_t sandwich(const SandwichArgs &A) {
-    if (use_rows && c.n <= kRowsMaxQubits && row_tiles(c.n, A.b.m).first * A.b.d <= 32) {
+    const bool rows_ok = c.n <= kRowsMaxQubits && row_tiles(c.n, A.b.m).first * A.b.d <= 32;
+    int kind = sw_kind;
+    if (kind == 0) kind = A.b.d <= 4 ? 3 : (rows_ok ? 1 : 2);
+    if (kind == 3 && A.b.d > 4) kind = rows_ok ? 1 : 2;
+    if (kind == 1 && !rows_ok) kind = 2;
+    if (kind == 3) return A.b.d == 2 ? launch_reg<2>(A) : launch_reg<4>(A);
+    if (kind == 1) {
       switch (A.b.d) {
         case 2: return launch_rows<2>(A);
         case 4: return launch_rows<4>(A);

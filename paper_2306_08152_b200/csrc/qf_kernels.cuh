@@ -318,7 +318,6 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
   const int p = lane / D, i = lane % D;
   const bool act = p < D / 2;
   for (int sweep = 0; sweep < 40; sweep++) {
-    bool any = false;
     for (int rd = 0; rd < D - 1; rd++) {
       int cp = 0, cq = 1;
       if (act) rr_pair<D>(rd, p, cp, cq);
@@ -345,15 +344,21 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
       // rotate iff |gamma| > 1e-15 sqrt(alpha beta)  (squared: no sqrt)
       const bool rot = act && g2 > 0.0 && g2 > 1e-30 * (al * be);
       if (rot) {
-        // e^{-i phi} = conj(gamma)/|gamma| makes the 2x2 Gram real; then the
-        // symmetric Schur rotation (Golub & Van Loan 8.4.1) with
-        // zeta = y / (2g), y = beta - alpha, written without the divisions:
-        // t = sign(y) 2g / (|y| + sqrt(4 g^2 + y^2)), c = 1/sqrt(1+t^2).
+        // e^{-i phi} = conj(gamma)/|gamma| (exactly unit modulus, fp64) makes the
+        // 2x2 Gram real; then the symmetric Schur rotation (Golub & Van Loan
+        // 8.4.1): t = sign(y) x / (|y| + sqrt(x^2 + y^2)), x = 2|gamma|,
+        // y = beta - alpha.  t only steers convergence, so it is formed in
+        // fp32 after an exact power-of-two rescale; c = 1/sqrt(1+t^2) and
+        // s = c t in fp64 keep the rotation unitary to fp64 rounding.
         const double inv_g = rsqrt(g2);
-        const double g = g2 * inv_g;
+        const double x = 2.0 * g2 * inv_g;
         const double y = be - al;
-        const double r = sqrt(fma(4.0, g2, y * y));
-        const double t = (y >= 0.0 ? 2.0 * g : -2.0 * g) / (fabs(y) + r);
+        const double m = fmax(x, fabs(y));
+        const long long eb = (__double_as_longlong(m) >> 52) & 0x7ff;
+        const double sc = __longlong_as_double((long long)(2046 - eb) << 52);  // ~1/m, exact 2^k
+        const float xf = (float)(x * sc), yf = (float)(y * sc);
+        const float tf = copysignf(xf, yf) / (fabsf(yf) + sqrtf(fmaf(xf, xf, yf * yf)));
+        const double t = (double)tf;
         const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
         const double2 ph = make_double2(ga.x * inv_g, -ga.y * inv_g);
         const double2 aq2 = cmul(aq, ph), vq2 = cmul(vq, ph);
@@ -362,10 +367,28 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
         Vm[i * D + cp] = make_double2(c * vp.x - s * vq2.x, c * vp.y - s * vq2.y);
         Vm[i * D + cq] = make_double2(s * vp.x + c * vq2.x, s * vp.y + c * vq2.y);
       }
-      any |= __any_sync(0xffffffffu, rot);
       __syncwarp();
     }
-    if (!any) break;
+    // convergence: every column pair orthogonal to 1e-15 relative, checked on
+    // the full Gram matrix at once (one parallel step instead of a no-op sweep)
+    bool bad_pair = false;
+    for (int o = lane; o < D * D; o += 32) {
+      const int pp = o / D, qq = o % D;
+      if (pp < qq) {
+        double2 gpq = make_double2(0.0, 0.0);
+        double npp = 0.0, nqq = 0.0;
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+          const double2 u = Am[r * D + pp], v = Am[r * D + qq];
+          gpq = cfma_cj(u, v, gpq);
+          npp = fma(u.x, u.x, fma(u.y, u.y, npp));
+          nqq = fma(v.x, v.x, fma(v.y, v.y, nqq));
+        }
+        const double q2 = cabs2(gpq);
+        bad_pair |= q2 > 0.0 && q2 > 1e-30 * (npp * nqq);
+      }
+    }
+    if (!__any_sync(0xffffffffu, bad_pair)) break;
   }
   // column norms -> X = A V / sigma (in place in Am)
   double sig = 0.0;
@@ -881,6 +904,91 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
     ptx::fence_proxy_async_smem();
     csync();
     if (tid == 0) ptx::mbar_arrive(&computed[st]);
+  }
+}
+
+// ------------------------------------------------------------------ register-block sandwich
+// k_sandwich_reg (d <= 4): each thread owns one d x d block (row-rest r,
+// column-rest c) of one start -- rows ins(a, r), columns ins(b, c) -- loads
+// it straight from global memory into registers (d^2 independent 16-byte
+// loads), applies ct <- E(L) ct E(R) and stores it back.  No shared-memory
+// staging of the tensor and no barriers in the steady state; lanes run over
+// consecutive c so every load/store instruction of a warp covers 32
+// consecutive elements when the location's bits are not the lowest ones.
+// A CTA handles 256 consecutive blocks of one start per chunk.
+template <int D>
+__global__ void __launch_bounds__(256) k_sandwich_reg(const SandwichArgs A) {
+  __shared__ double2 Ls[D * D], Rs[D * D];
+  const int N = A.N, NR = N / D;
+  const int bps = NR * NR;                      // blocks per start
+  const int cps = (bps + 255) / 256;            // chunks per start
+  const int nact = *A.n_active;
+  const long long total = (long long)nact * cps;
+  const long long per = (total + gridDim.x - 1) / gridDim.x;
+  const long long c0 = (long long)blockIdx.x * per;
+  const long long c1 = c0 + per < total ? c0 + per : total;
+  const bool has_r = A.rsrc != nullptr;
+  const int tid = threadIdx.x;
+  int cur = -1;
+  for (long long ch = c0; ch < c1; ch++) {
+    const int ai = (int)(ch / cps);
+    const int s = A.active[ai];
+    if (s != cur) {  // CTA-uniform
+      __syncthreads();
+      if (tid < D * D) {
+        const double2 *L = A.lsrc + (long long)s * A.lstride;
+        const int i = tid / D, k = tid % D;
+        Ls[tid] = A.ldag ? cconj(L[k * D + i]) : L[tid];
+        if (has_r) {
+          const double2 *R = A.rsrc + (long long)s * A.rstride;
+          Rs[tid] = A.rdag ? cconj(R[k * D + i]) : R[tid];
+        }
+      }
+      cur = s;
+      __syncthreads();
+    }
+    const int bi = (int)(ch - (long long)ai * cps) * 256 + tid;
+    if (bi >= bps) continue;
+    const int r = bi / NR, c = bi - (bi / NR) * NR;
+    const int rb = spread_rest(A.b, r), cb = spread_rest(A.b, c);
+    double2 *cts = A.ct + (long long)s * A.ct_stride;
+    double2 x[D][D];
+#pragma unroll
+    for (int a = 0; a < D; a++)
+#pragma unroll
+      for (int b = 0; b < D; b++)
+        x[a][b] = cts[(long long)(rb | A.b.abits[a]) * N + (cb | A.b.abits[b])];
+    // left: column by column, in place in registers
+#pragma unroll
+    for (int b = 0; b < D; b++) {
+      double2 t[D];
+#pragma unroll
+      for (int a = 0; a < D; a++) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k][b], acc);
+        t[a] = acc;
+      }
+#pragma unroll
+      for (int a = 0; a < D; a++) x[a][b] = t[a];
+    }
+    // right: row by row, straight to global memory
+#pragma unroll
+    for (int a = 0; a < D; a++) {
+      double2 *row = cts + (long long)(rb | A.b.abits[a]) * N + cb;
+      if (has_r) {
+#pragma unroll
+        for (int b = 0; b < D; b++) {
+          double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < D; k++) z = cfma(x[a][k], Rs[k * D + b], z);
+          row[A.b.abits[b]] = z;
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < D; b++) row[A.b.abits[b]] = x[a][b];
+      }
+    }
   }
 }
 
