@@ -338,7 +338,8 @@ struct Engine {
   // sandwich kernel choice: 0 auto (d <= 4: register blocks; d = 8: TMA row
   // tiles up to n = 9, else smem tiles); QF_SANDWICH=rows|tile|reg forces one
   int sw_kind = 0;
-  bool warm = true;      // QF_WARM=0 disables the warm-started Jacobi (A/B runs)
+  bool warm = false;     // QF_WARM=1: warm-started Jacobi polar (A/B runs)
+  bool polar_jacobi = false;  // QF_POLAR=jacobi: Jacobi polar instead of Newton-Schulz
   std::vector<int> voff; // per gate: complex offset of its backward slot in vstore
   long long launches = 0;
   int sandwich_grid[4] = {0, 0, 0, 0};
@@ -369,7 +370,8 @@ struct Engine {
       const std::string v(e);
       sw_kind = v == "rows" ? 1 : v == "tile" ? 2 : v == "reg" ? 3 : 0;
     }
-    if (const char *e = getenv("QF_WARM")) warm = std::string(e) != "0";
+    if (const char *e = getenv("QF_WARM")) warm = std::string(e) == "1";
+    if (const char *e = getenv("QF_POLAR")) polar_jacobi = std::string(e) == "jacobi";
     voff.assign(c.p, -1);
     long long o = 0;
     for (int k = 0; k < c.p; k++)
@@ -536,6 +538,7 @@ struct Engine {
     A.scratch = scratch();
     A.forward = forward;
     A.beta = p.beta;
+    A.polar_jacobi = polar_jacobi ? 1 : 0;
     if (warm) {
       A.vstore = reinterpret_cast<double2 *>(ws + L.vstore);
       A.vstride = L.vstride;
@@ -842,6 +845,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.vstore = E.warm ? reinterpret_cast<double2 *>(W + E.L.vstore) : nullptr;
     A.vstride = E.L.vstride;
     A.counter = counter;
+    A.polar_jacobi = E.polar_jacobi ? 1 : 0;
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;
     A.diff_tol_r = p.diff_tol_r;

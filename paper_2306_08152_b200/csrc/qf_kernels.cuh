@@ -24,6 +24,9 @@
 namespace qf {
 
 constexpr int kMaxQubits = 12;
+#ifdef QF_POLAR_COUNT
+__device__ unsigned long long qf_polar_sweeps;  // microbenchmark instrumentation only
+#endif
 constexpr int kTileItems = 256;   // work items per sandwich tile (= threads)
 constexpr int kScratch = 64;      // complex per start in the u_old scratch
 
@@ -217,6 +220,7 @@ struct EnvArgs {
   double2 *vstore;      // warm-start right singular vectors (nullptr: cold Jacobi)
   long long vstride;    // complex per start
   int voff;             // complex offset of (gate, direction)
+  int polar_jacobi;     // 1: one-sided Jacobi instead of Newton-Schulz
 };
 
 // Round-robin (circle method) pairing for a parallel-ordered Jacobi sweep:
@@ -238,8 +242,8 @@ __device__ __forceinline__ void rr_pair(int rd, int p, int &cp, int &cq) {
 // A v0 with V = v0, which is already nearly column-orthogonal once the
 // optimisation settles; the polar factor is unique, so only rounding differs.
 template <int D>
-__device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
-                           const double2 *v0 = nullptr) {
+__device__ void warp_polar_jacobi(double2 *Am, double2 *Vm, double2 *U, int lane,
+                                  const double2 *v0 = nullptr) {
   if constexpr (D == 2) {
     if (lane == 0) {
       const double2 a = Am[0], b = Am[1], c = Am[2], e = Am[3];
@@ -266,8 +270,10 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
     __syncwarp();
   } else {
   if (v0) {
-    for (int e = lane; e < D * D; e += 32) Vm[e] = v0[e];
-    __syncwarp();
+    if (v0 != Vm) {  // (v0 == Vm: the caller already placed V0 in Vm)
+      for (int e = lane; e < D * D; e += 32) Vm[e] = v0[e];
+      __syncwarp();
+    }
     // re-unitarise the stored V with one Newton-Schulz step,
     // V <- V (3I - V^H V) / 2, so rounding drift does not accumulate across
     // reuses (unitarity error e -> O(e^2)); U is scratch here
@@ -344,28 +350,44 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
       // rotate iff |gamma| > 1e-15 sqrt(alpha beta)  (squared: no sqrt)
       const bool rot = act && g2 > 0.0 && g2 > 1e-30 * (al * be);
       if (rot) {
-        // e^{-i phi} = conj(gamma)/|gamma| (exactly unit modulus, fp64) makes the
-        // 2x2 Gram real; then the symmetric Schur rotation (Golub & Van Loan
-        // 8.4.1): t = sign(y) x / (|y| + sqrt(x^2 + y^2)), x = 2|gamma|,
-        // y = beta - alpha.  t only steers convergence, so it is formed in
-        // fp32 after an exact power-of-two rescale; c = 1/sqrt(1+t^2) and
-        // s = c t in fp64 keep the rotation unitary to fp64 rounding.
-        const double inv_g = rsqrt(g2);
-        const double x = 2.0 * g2 * inv_g;
+        // Jacobi rotation J = [[c, s'], [-conj(s'), c]] that zeroes the 2x2
+        // Gram [[alpha, gamma], [conj(gamma), beta]] of columns (p, q):
+        // tan(theta) = t = sign(y) x / (|y| + sqrt(x^2 + y^2)), x = 2|gamma|,
+        // y = beta - alpha (Golub & Van Loan 8.4.1), s' = sin(theta) gamma/|gamma|.
+        // The angle only steers convergence, so it is formed in fp32 (fast
+        // MUFU intrinsics, after an exact power-of-two rescale); the rotation
+        // applied is exactly unitary to fp64 rounding by the Cayley form
+        // sigma = tan(theta/2) e^{i phi}: c = (1-|sigma|^2)/(1+|sigma|^2),
+        // s' = 2 sigma/(1+|sigma|^2)  (one fp64 division).
         const double y = be - al;
-        const double m = fmax(x, fabs(y));
+        const double m = fmax(fmax(fabs(ga.x), fabs(ga.y)), fabs(y));
         const long long eb = (__double_as_longlong(m) >> 52) & 0x7ff;
         const double sc = __longlong_as_double((long long)(2046 - eb) << 52);  // ~1/m, exact 2^k
-        const float xf = (float)(x * sc), yf = (float)(y * sc);
-        const float tf = copysignf(xf, yf) / (fabsf(yf) + sqrtf(fmaf(xf, xf, yf * yf)));
-        const double t = (double)tf;
-        const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
-        const double2 ph = make_double2(ga.x * inv_g, -ga.y * inv_g);
-        const double2 aq2 = cmul(aq, ph), vq2 = cmul(vq, ph);
-        Am[i * D + cp] = make_double2(c * ap.x - s * aq2.x, c * ap.y - s * aq2.y);
-        Am[i * D + cq] = make_double2(s * ap.x + c * aq2.x, s * ap.y + c * aq2.y);
-        Vm[i * D + cp] = make_double2(c * vp.x - s * vq2.x, c * vp.y - s * vq2.y);
-        Vm[i * D + cq] = make_double2(s * vp.x + c * vq2.x, s * vp.y + c * vq2.y);
+        const float gx = (float)(ga.x * sc), gy = (float)(ga.y * sc), yf = (float)(y * sc);
+        const float g2f = fmaf(gx, gx, gy * gy);
+        const float rg = g2f > 0.0f ? rsqrtf(g2f) : 0.0f;
+        const float xf = 2.0f * g2f * rg;
+        const float rr = fmaf(xf, xf, yf * yf);
+        const float tf = __fdividef(copysignf(xf, yf), fabsf(yf) + rr * rsqrtf(rr));
+        // tan(theta/2) = t / (1 + sqrt(1 + t^2))
+        const float q2 = fmaf(tf, tf, 1.0f);
+        const float hf = __fdividef(tf, 1.0f + q2 * rsqrtf(q2));
+        const double sgx = (double)(hf * gx * rg), sgy = (double)(hf * gy * rg);  // sigma
+        const double n2 = fma(sgx, sgx, sgy * sgy);
+        // (g2f == 0: gamma below fp32 range next to |beta - alpha|, the angle is
+        //  ~0 -- sigma = 0 makes J = I)
+        const double inv = g2f > 0.0f ? 1.0 / (1.0 + n2) : 0.0;
+        const double c = g2f > 0.0f ? (1.0 - n2) * inv : 1.0;
+        const double2 sp = make_double2(2.0 * sgx * inv, 2.0 * sgy * inv);  // s'
+        // a_p' = c a_p - conj(s') a_q,  a_q' = s' a_p + c a_q  (same for V)
+        Am[i * D + cp] = make_double2(c * ap.x - (sp.x * aq.x + sp.y * aq.y),
+                                      c * ap.y - (sp.x * aq.y - sp.y * aq.x));
+        Am[i * D + cq] = make_double2(c * aq.x + (sp.x * ap.x - sp.y * ap.y),
+                                      c * aq.y + (sp.x * ap.y + sp.y * ap.x));
+        Vm[i * D + cp] = make_double2(c * vp.x - (sp.x * vq.x + sp.y * vq.y),
+                                      c * vp.y - (sp.x * vq.y - sp.y * vq.x));
+        Vm[i * D + cq] = make_double2(c * vq.x + (sp.x * vp.x - sp.y * vp.y),
+                                      c * vq.y + (sp.x * vp.y + sp.y * vp.x));
       }
       __syncwarp();
     }
@@ -388,6 +410,9 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
         bad_pair |= q2 > 0.0 && q2 > 1e-30 * (npp * nqq);
       }
     }
+#ifdef QF_POLAR_COUNT
+    if (lane == 0) atomicAdd(&qf_polar_sweeps, 1);
+#endif
     if (!__any_sync(0xffffffffu, bad_pair)) break;
   }
   // column norms -> X = A V / sigma (in place in Am)
@@ -452,6 +477,134 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
   }
   __syncwarp();
   }  // D > 2
+}
+
+// C = op(A) B for D x D complex matrices in warp shared memory, lanes over the
+// outputs (fixed summation order); conjA: C = A^H B.
+template <int D, bool conjA>
+__device__ __forceinline__ void warp_mm(const double2 *Am, const double2 *Bm, double2 *out,
+                                        int lane) {
+  constexpr int OPL = (D * D + 31) / 32;
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+    const int o = lane + 32 * q;
+    if (o < D * D) {
+      const int r = o / D, c = o % D;
+      // two interleaved accumulators halve the dependent FMA chain
+      double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0;
+#pragma unroll
+      for (int k = 0; k < D; k += 2) {
+        acc0 = conjA ? cfma_cj(Am[k * D + r], Bm[k * D + c], acc0)
+                     : cfma(Am[r * D + k], Bm[k * D + c], acc0);
+        acc1 = conjA ? cfma_cj(Am[(k + 1) * D + r], Bm[(k + 1) * D + c], acc1)
+                     : cfma(Am[r * D + k + 1], Bm[(k + 1) * D + c], acc1);
+      }
+      out[o] = cadd(acc0, acc1);
+    }
+  }
+}
+
+// Unitary polar factor by the quintic Newton-Schulz iteration
+//   X <- X (15 I - 10 Y + 3 Y^2) / 8,   Y = X^H X,   X_0 = A / ||A||_F,
+// which keeps the singular vectors of A and drives every singular value in
+// (0, 1] to 1 (growth 15/8 per step while small, cubic convergence near 1).
+// Every step is three small matrix products done by all lanes at once, so its
+// latency is a few hundred cycles against ~1000 per Jacobi round.  Stops one
+// step after max |Y - I| <= 1e-5 (error then ~(1e-5)^3).  Returns false if it
+// has not converged after 48 steps (A singular or near it); X (in Am) then
+// still has the polar factor of A and the caller finishes with Jacobi.
+// Buffers: X in Am (in place), Y in Ym, Z / W in Wm; result copied to U.
+template <int D>
+__device__ bool warp_polar_ns(double2 *Am, double2 *Ym, double2 *Wm, double2 *U, int lane) {
+  constexpr int DD = D * D, OPL = (DD + 31) / 32;
+  double f = 0.0;
+#pragma unroll
+  for (int q = 0; q < OPL; q++)
+    if (lane + 32 * q < DD) f += cabs2(Am[lane + 32 * q]);
+  for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
+  if (!(f > 0.0) || !isfinite(f)) return false;
+  const double sc = rsqrt(f);
+#pragma unroll
+  for (int q = 0; q < OPL; q++)
+    if (lane + 32 * q < DD) Am[lane + 32 * q] = cscale(Am[lane + 32 * q], sc);
+  __syncwarp();
+  bool done = false, fast = true;
+  for (int it = 0; it < 48 && !done; it++) {
+    warp_mm<D, true>(Am, Am, Ym, lane);  // Y = X^H X
+    double dev = 0.0;
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {
+      const int o = lane + 32 * q;
+      if (o < DD) {
+        const double2 y = Ym[o];
+        const double dx = y.x - (o / D == o % D ? 1.0 : 0.0);
+        dev = fmax(dev, fmax(fabs(dx), fabs(y.y)));
+        if (!(dx == dx && y.y == y.y)) dev = INFINITY;
+      }
+    }
+    done = !__any_sync(0xffffffffu, !(dev <= 1e-5));
+    // while some singular value may still be far from 1, take the steeper
+    // quintic p(s) = 3.4445 s - 4.7750 s^3 + 2.0315 s^5 (maps (0, 1.2] into
+    // (0, 1.2], slope 3.44 at 0); then the exact one, whose fixed point is 1
+    // (the steep map leaves s in [0.68, 1.2], i.e. |s^2 - 1| <= 0.54: switch
+    //  once every entry of Y - I is inside that band, or after 8 steps)
+    if (fast) fast = it < 8 && __any_sync(0xffffffffu, !(dev <= 0.55));
+    const double ca = fast ? 3.4445 : 1.875, cb = fast ? -4.7750 : -1.25,
+                 cc = fast ? 2.0315 : 0.375;
+    __syncwarp();
+    warp_mm<D, false>(Ym, Ym, Wm, lane);  // Z = Y^2
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {  // W = ca I + cb Y + cc Z  (exact: (15 - 10 Y + 3 Z) / 8)
+      const int o = lane + 32 * q;
+      if (o < DD) {
+        const double2 y = Ym[o], z = Wm[o];
+        Wm[o] = make_double2(fma(cc, z.x, fma(cb, y.x, o / D == o % D ? ca : 0.0)),
+                             fma(cc, z.y, cb * y.y));
+      }
+    }
+    __syncwarp();
+    double2 xw[OPL];  // X <- X W, staged in registers (X is read by all lanes)
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {
+      const int o = lane + 32 * q;
+      xw[q] = make_double2(0.0, 0.0);
+      if (o < DD) {
+        const int r = o / D, c = o % D;
+#pragma unroll
+        for (int k = 0; k < D; k++) xw[q] = cfma(Am[r * D + k], Wm[k * D + c], xw[q]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < OPL; q++)
+      if (lane + 32 * q < DD) Am[lane + 32 * q] = xw[q];
+    __syncwarp();
+  }
+  if (done)
+#pragma unroll
+    for (int q = 0; q < OPL; q++)
+      if (lane + 32 * q < DD) U[lane + 32 * q] = Am[lane + 32 * q];
+  __syncwarp();
+  return done;
+}
+
+// Polar factor dispatcher: closed form for 2 x 2; for 4 x 4 and 8 x 8 the
+// Newton-Schulz iteration with a Jacobi finish when it does not converge
+// (near-singular A), or Jacobi alone when `jacobi` is set or a warm start v0
+// is supplied.  Am, Vm are scratch; the result goes to U.
+template <int D>
+__device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
+                           const double2 *v0 = nullptr, bool jacobi = false) {
+  if constexpr (D == 2) {
+    warp_polar_jacobi<D>(Am, Vm, U, lane, nullptr);
+  } else {
+    if (jacobi || v0 != nullptr) {
+      warp_polar_jacobi<D>(Am, Vm, U, lane, v0);
+    } else if (!warp_polar_ns<D>(Am, Vm, U, U, lane)) {
+      warp_polar_jacobi<D>(Am, Vm, U, lane, nullptr);
+    }
+  }
 }
 
 constexpr int kEnvWarps = 4;
@@ -538,7 +691,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
     }
     __syncwarp();
     double2 *vs = (A.vstore && D > 2) ? A.vstore + (long long)s * A.vstride + A.voff : nullptr;
-    warp_polar<D>(Am, Vm, Pm, lane, vs);
+    warp_polar<D>(Am, Vm, Pm, lane, vs, A.polar_jacobi != 0);
     if (vs)
       for (int e = lane; e < DD; e += 32) vs[e] = Vm[e];
     double2 *sc = A.scratch + (long long)s * kScratch;

@@ -35,6 +35,7 @@ struct ResidentArgs {
   double2 *vstore;    // nullptr: cold Jacobi
   long long vstride;
   int *counter;       // work-stealing start counter (zeroed before launch)
+  int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
   double dist_tol, diff_tol_a, diff_tol_r, long_diff_r, beta;
   int long_diff_count, min_iters, max_iters, reset_iters, ring;
   double *hist;
@@ -50,7 +51,9 @@ struct ResidentArgs {
 
 __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
   int x = 0;
-  for (int k = 0; k < n - g.m; k++) x |= ((r >> k) & 1) << g.rest_pos[k];
+#pragma unroll
+  for (int k = 0; k < kMaxQubits; k++)
+    if (k < n - g.m) x |= ((r >> k) & 1) << g.rest_pos[k];
   return x;
 }
 
@@ -145,19 +148,48 @@ __device__ void res_update(const ResidentArgs &A, const double2 *ct, const GateD
                            double2 *u, double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm,
                            double2 *vs, int forward, int lane) {
   constexpr int DD = D * D;
+  constexpr int SPLIT = DD >= 32 ? 1 : 32 / DD;  // lanes per output
+  constexpr int OPL = DD >= 32 ? DD / 32 : 1;    // outputs per lane
   const int N = A.N, R = N / D;
-  for (int e = lane; e < DD; e += 32) Uo[e] = u[e];
-  // P[a][b] = sum_r ct[ins(a,r)][ins(b,r)], r ascending per output
-  for (int o = lane; o < DD; o += 32) {
+  // global loads first (u_old, the warm-start V): they overlap the gather
+  double2 ureg[OPL], vreg[OPL];
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+    const int e = lane + 32 * q;
+    if (e < DD) {
+      ureg[q] = u[e];
+      if (vs) vreg[q] = vs[e];
+    }
+  }
+  // P[a][b] = sum_r ct[ins(a,r)][ins(b,r)]: SPLIT lanes per output take
+  // r = k, k+SPLIT, ... ascending, then a fixed xor-tree combines them
+  const int k = lane % SPLIT;
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+    const int o = lane / SPLIT + q * (32 / SPLIT);
     const int a = o / D, b = o % D;
     double2 acc = make_double2(0.0, 0.0);
-    for (int r = 0; r < R; r++) {
-      const int sp = rspread(g, A.n, r);
-      const double2 v = ct[(sp | g.abits[a]) * N + (sp | g.abits[b])];
-      acc.x += v.x;
-      acc.y += v.y;
+    if (o < DD)
+      for (int r = k; r < R; r += SPLIT) {
+        const int sp = rspread(g, A.n, r);
+        const double2 v = ct[(sp | g.abits[a]) * N + (sp | g.abits[b])];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+#pragma unroll
+    for (int off = 1; off < SPLIT; off <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
     }
-    Pm[o] = acc;
+    if (k == 0 && o < DD) Pm[o] = acc;
+  }
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+    const int e = lane + 32 * q;
+    if (e < DD) {
+      Uo[e] = ureg[q];
+      if (vs) Vm[e] = vreg[q];  // warm-start V0, already in place for warp_polar
+    }
   }
   __syncwarp();
   for (int o = lane; o < DD; o += 32) {
@@ -184,7 +216,7 @@ __device__ void res_update(const ResidentArgs &A, const double2 *ct, const GateD
     Am[o] = acc;
   }
   __syncwarp();
-  warp_polar<D>(Am, Vm, Pm, lane, vs);  // u_new -> Pm
+  warp_polar<D>(Am, Vm, Pm, lane, vs ? Vm : nullptr, A.polar_jacobi != 0);  // u_new -> Pm
   if (vs)
     for (int e = lane; e < DD; e += 32) vs[e] = Vm[e];
   for (int e = lane; e < DD; e += 32) u[e] = Pm[e];

@@ -2,6 +2,7 @@
 // warm-started, in SM clock cycles (clock64), one warp per CTA.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2306_08152_b200/csrc \
 //        -I include -o /tmp/polar_bench tools/polar_bench.cu
+#define QF_POLAR_COUNT 1
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -28,8 +29,11 @@ __global__ void bench(const double2 *A0, const double2 *A1, long long *cyc, doub
       Am[e] = a1[e];
     }
     __syncwarp();
+    for (int e = lane; e < D * D; e += 32) V0[e] = U[e];  // NS result
+    for (int e = lane; e < D * D; e += 32) Am[e] = a0[e];
+    __syncwarp();
     t0 = clock64();
-    warp_polar<D>(Am, Vm, U, lane, V0);
+    warp_polar<D>(Am, Vm, U, lane, nullptr, true);  // Jacobi
     t1 = clock64();
     tw += t1 - t0;
   }
@@ -37,13 +41,14 @@ __global__ void bench(const double2 *A0, const double2 *A1, long long *cyc, doub
     cyc[2 * blockIdx.x] = tc / reps;
     cyc[2 * blockIdx.x + 1] = tw / reps;
   }
-  // unitarity error of the warm result
+  // unitarity error of the NS result (V0) and its distance to the Jacobi result (U)
   double e = 0.0;
   for (int o = lane; o < D * D; o += 32) {
     const int i = o / D, j = o % D;
     double2 acc = make_double2(i == j ? -1.0 : 0.0, 0.0);
-    for (int k = 0; k < D; k++) acc = cfma_cj(U[k * D + i], U[k * D + j], acc);
+    for (int k = 0; k < D; k++) acc = cfma_cj(V0[k * D + i], V0[k * D + j], acc);
     e = fmax(e, fmax(fabs(acc.x), fabs(acc.y)));
+    e = fmax(e, fmax(fabs(V0[o].x - U[o].x), fabs(V0[o].y - U[o].y)));
   }
   for (int off = 16; off; off >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
   if (lane == 0) err[blockIdx.x] = e;
@@ -67,8 +72,11 @@ void run(int blocks) {
   cudaMalloc(&err, blocks * sizeof(double));
   cudaMemcpy(d0, h0, n * sizeof(double2), cudaMemcpyHostToDevice);
   cudaMemcpy(d1, h1, n * sizeof(double2), cudaMemcpyHostToDevice);
+  unsigned long long zero = 0, sweeps = 0;
+  cudaMemcpyToSymbol(qf_polar_sweeps, &zero, sizeof(zero));
   bench<D><<<blocks, 32>>>(d0, d1, cyc, err, 10);
   cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&sweeps, qf_polar_sweeps, sizeof(sweeps));
   long long *hc = (long long *)malloc(2 * blocks * sizeof(long long));
   double *he = (double *)malloc(blocks * sizeof(double));
   cudaMemcpy(hc, cyc, 2 * blocks * sizeof(long long), cudaMemcpyDeviceToHost);
@@ -79,8 +87,9 @@ void run(int blocks) {
     w += hc[2 * b + 1];
     e = e > he[b] ? e : he[b];
   }
-  printf("D=%d: cold %.0f cycles, warm %.0f cycles, max unitarity err %.2e  (%s)\n", D, c / blocks,
-         w / blocks, e, cudaGetErrorString(cudaGetLastError()));
+  printf("D=%d: NS %.0f cycles, Jacobi %.0f cycles, Jacobi sweeps/call %.2f, max(unitarity err, |NS-Jacobi|) "
+         "%.2e  (%s)\n", D, c / blocks, w / blocks, sweeps / (10.0 * blocks), e,
+         cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
