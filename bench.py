@@ -231,6 +231,8 @@ def main():
     ap.add_argument("--max-iters", type=int, default=None,
                     help="override the config's max_iters (not for reported numbers)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--engine", default="auto", choices=["auto", "stream", "resident"],
+                    help="device engine (auto: resident for n <= 6)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
@@ -247,6 +249,8 @@ def main():
     import paper_2306_08152_b200 as qf
     from paper_2306_08152_b200 import dist as qfdist
 
+    engine = {"auto": qf.QF_ENGINE_AUTO, "stream": qf.QF_ENGINE_STREAM,
+              "resident": qf.QF_ENGINE_RESIDENT}[args.engine]
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -267,7 +271,8 @@ def main():
 
     def step(profile):
         r = qf.qf_instantiate_device(c, d_V, d_init, ws, stream, d_gates_out=gates_out,
-                                     d_summary_out=summ, max_iters=w.max_iters, profile=profile)
+                                     d_summary_out=summ, max_iters=w.max_iters, profile=profile,
+                                     engine=engine)
         best = qfdist.exchange_best(shard, summ, gates_out, stream) if world > 1 else None
         return r, best
 
@@ -315,11 +320,13 @@ def main():
         h_V = torch.from_numpy(V.view(np.float64).copy()).pin_memory()
         h_init = torch.from_numpy(init).pin_memory()
         for _ in range(1):
-            qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters)
+            qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters,
+                                  engine=engine)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        rr = [qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters)
+        rr = [qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters,
+                                    engine=engine)
               for _ in range(args.steps)]
         t_e2e = time.perf_counter() - t0
         tv = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
