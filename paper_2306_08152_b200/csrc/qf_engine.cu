@@ -846,6 +846,8 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.vstride = E.L.vstride;
     A.counter = counter;
     A.polar_jacobi = E.polar_jacobi ? 1 : 0;
+    A.pipelined = 0;
+    if (const char *e = getenv("QF_PIPELINE")) A.pipelined = std::string(e) == "1";
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;
     A.diff_tol_r = p.diff_tol_r;
@@ -866,7 +868,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.rec_gates = reinterpret_cast<double *>(W + E.L.rec_gates);
     A.var_doubles = c.var_doubles;
     const int threads = resident_threads(c.n);
-    const size_t smem = (size_t)N * N * 16 + 6 * 64 * 16;
+    const size_t smem = (size_t)N * N * 16 + 8 * 64 * 16;
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
     auto kern = maxm == 1 ? k_resident<2> : maxm == 2 ? k_resident<4> : k_resident<8>;
@@ -1029,3 +1031,13 @@ qf_status select_best_device(const qf_summary *d, long long count, cudaStream_t 
 }
 
 }  // namespace qf
+
+#ifdef QF_POLAR_COUNT
+// debug build only (tools/polar_stats.py): polar-factor iteration counters
+extern "C" void qf_debug_polar_counts(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&out[0], qf::qf_ns_calls, 8);
+  cudaMemcpyFromSymbol(&out[1], qf::qf_ns_iters, 8);
+  cudaMemcpyFromSymbol(&out[2], qf::qf_polar_sweeps, 8);
+}
+#endif

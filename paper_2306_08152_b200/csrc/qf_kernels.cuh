@@ -26,6 +26,7 @@ namespace qf {
 constexpr int kMaxQubits = 12;
 #ifdef QF_POLAR_COUNT
 __device__ unsigned long long qf_polar_sweeps;  // microbenchmark instrumentation only
+__device__ unsigned long long qf_ns_iters, qf_ns_calls;
 #endif
 constexpr int kTileItems = 256;   // work items per sandwich tile (= threads)
 constexpr int kScratch = 64;      // complex per start in the u_old scratch
@@ -529,8 +530,39 @@ __device__ bool warp_polar_ns(double2 *Am, double2 *Ym, double2 *Wm, double2 *U,
     if (lane + 32 * q < DD) Am[lane + 32 * q] = cscale(Am[lane + 32 * q], sc);
   __syncwarp();
   bool done = false, fast = true;
+#ifdef QF_POLAR_COUNT
+  if (lane == 0) atomicAdd(&qf_ns_calls, 1ull);
+#endif
   for (int it = 0; it < 48 && !done; it++) {
+#ifdef QF_POLAR_COUNT
+    if (lane == 0) atomicAdd(&qf_ns_iters, 1ull);
+#endif
     warp_mm<D, true>(Am, Am, Ym, lane);  // Y = X^H X
+    if (it == 0) {
+      // rescale so that sigma_max(X) <= 1 tightly: lambda_max(Y) <= the largest
+      // absolute row sum of Y (Gershgorin).  A near-unitary A then starts at
+      // Y ~ I instead of Y ~ I/D.  Max over lanes on the high words of the
+      // non-negative doubles (ordered like the values), padded by 1e-5.
+      __syncwarp();
+      double rs = 0.0;
+      if (lane < D) {
+#pragma unroll
+        for (int k = 0; k < D; k++) rs += fabs(Ym[lane * D + k].x) + fabs(Ym[lane * D + k].y);
+      }
+      const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(rs) >> 32));
+      const double gmax = __longlong_as_double((long long)(hi + 1u) << 32);  // >= every rs
+      const double s1 = rsqrt(gmax * (1.0 + 1e-5)), s2 = s1 * s1;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < OPL; q++) {
+        const int o = lane + 32 * q;
+        if (o < DD) {
+          Am[o] = cscale(Am[o], s1);
+          Ym[o] = cscale(Ym[o], s2);
+        }
+      }
+      __syncwarp();
+    }
     double dev = 0.0;
 #pragma unroll
     for (int q = 0; q < OPL; q++) {

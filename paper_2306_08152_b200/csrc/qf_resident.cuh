@@ -36,6 +36,7 @@ struct ResidentArgs {
   long long vstride;
   int *counter;       // work-stealing start counter (zeroed before launch)
   int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
+  int pipelined;      // 1: overlap the next gate's polar factor with this sandwich
   double dist_tol, diff_tol_a, diff_tol_r, long_diff_r, beta;
   int long_diff_count, min_iters, max_iters, reset_iters, ring;
   double *hist;
@@ -49,6 +50,17 @@ struct ResidentArgs {
   int var_doubles;
 };
 
+// Shared-memory layout of the resident tensor: element (i, j) at
+// i*N + swz(j), swz(j) = j ^ f(j >> 3 & 7) -- a bijection within each row that
+// spreads the strided column sets of low-bit gates over the 8 bank groups of
+// a 128-byte wavefront (f searched over all 1-3-qubit locations at n <= 6 for
+// the block thread mapping: 392 vs 840 wavefronts unswizzled at n = 6,
+// worst case 2-way instead of 8-way).
+__device__ __forceinline__ int swz(int j) {
+  return j ^ (int)((0x41362750u >> (4 * ((j >> 3) & 7))) & 7u);
+}
+__device__ __forceinline__ int sidx(int i, int j, int N) { return i * N + swz(j); }
+
 __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
   int x = 0;
 #pragma unroll
@@ -59,19 +71,24 @@ __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
 
 // ct <- E(L) ct E(R) in place for D <= 4, one D x D block (row-rest r,
 // column-rest c) per item held in registers: one shared-memory read and write
-// per element and a single barrier per step.
+// per element.  `mode` selects the blocks of the pipelined schedule (see
+// k_resident): 0 all, 1 those the next gate's environment reads
+// ((r ^ c) & ~dm == 0), 2 the others; items are spread over threads
+// t0, t0 + nt, ...  No barrier inside.
 template <int D>
 __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N,
-                                    const double2 *Ls, const double2 *Rs) {
+                                    const double2 *Ls, const double2 *Rs, int mode, int dm,
+                                    int t0, int nt) {
   const int NR = N / D;
-  for (int it = threadIdx.x; it < NR * NR; it += blockDim.x) {
+  for (int it = t0; it < NR * NR; it += nt) {
     const int r = it / NR, c = it - r * NR;
+    if (mode != 0 && (((r ^ c) & ~dm) == 0) != (mode == 1)) continue;
     const int rb = rspread(g, n, r), cb = rspread(g, n, c);
     double2 x[D][D];
 #pragma unroll
     for (int a = 0; a < D; a++)
 #pragma unroll
-      for (int b = 0; b < D; b++) x[a][b] = ct[(rb | g.abits[a]) * N + (cb | g.abits[b])];
+      for (int b = 0; b < D; b++) x[a][b] = ct[sidx(rb | g.abits[a], cb | g.abits[b], N)];
     // row by row: z[a][:] = (L[a][:] x) R, stored over the (register-held) block
 #pragma unroll
     for (int a = 0; a < D; a++) {
@@ -89,11 +106,10 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
         double2 z = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 0; k < D; k++) z = cfma(y[k], Rs[k * D + b], z);
-        ct[(rb | g.abits[a]) * N + (cb | g.abits[b])] = z;
+        ct[sidx(rb | g.abits[a], cb | g.abits[b], N)] = z;
       }
     }
   }
-  __syncthreads();
 }
 
 // ct <- E(L) ct E(R) in place (R == nullptr: one-sided), all threads.
@@ -108,13 +124,13 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
     const int rb = rspread(g, n, r);
     double2 x[D];
 #pragma unroll
-    for (int a = 0; a < D; a++) x[a] = ct[(rb | g.abits[a]) * N + j];
+    for (int a = 0; a < D; a++) x[a] = ct[sidx(rb | g.abits[a], j, N)];
 #pragma unroll
     for (int a = 0; a < D; a++) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k], acc);
-      ct[(rb | g.abits[a]) * N + j] = acc;
+      ct[sidx(rb | g.abits[a], j, N)] = acc;
     }
   }
   if (Rs == nullptr) {
@@ -129,13 +145,13 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
     double2 *row = ct + i * N;
     double2 z[D];
 #pragma unroll
-    for (int b = 0; b < D; b++) z[b] = row[cb | g.abits[b]];
+    for (int b = 0; b < D; b++) z[b] = row[swz(cb | g.abits[b])];
 #pragma unroll
     for (int b = 0; b < D; b++) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < D; k++) acc = cfma(z[k], Rs[k * D + b], acc);
-      row[cb | g.abits[b]] = acc;
+      row[swz(cb | g.abits[b])] = acc;
     }
   }
   __syncthreads();
@@ -172,7 +188,7 @@ __device__ void res_update(const ResidentArgs &A, const double2 *ct, const GateD
     if (o < DD)
       for (int r = k; r < R; r += SPLIT) {
         const int sp = rspread(g, A.n, r);
-        const double2 v = ct[(sp | g.abits[a]) * N + (sp | g.abits[b])];
+        const double2 v = ct[sidx(sp | g.abits[a], sp | g.abits[b], N)];
         acc.x += v.x;
         acc.y += v.y;
       }
@@ -223,55 +239,69 @@ __device__ void res_update(const ResidentArgs &A, const double2 *ct, const GateD
   __syncwarp();
 }
 
+// warp 0: the operands of gate step (g, forward) into (Lb, Rb).  VARIABLE:
+// environment from the resident tensor, polar update, u_new to global memory,
+// backward L = u_old^H, R = u_new / forward L = u_new, R = u_old^H
+// (P:599-605).  CONSTANT: the fixed matrix and its adjoint.
 template <int D>
-__device__ void res_step(const ResidentArgs &A, double2 *ct, const GateDesc &g, int s, int forward,
-                         double2 *Ls, double2 *Rs, double2 *Uo, double2 *Pm, double2 *Am,
-                         double2 *Vm) {
+__device__ void res_prepare_d(const ResidentArgs &A, const double2 *ct, const GateDesc &g, int s,
+                              int forward, double2 *Lb, double2 *Rb, double2 *Uo, double2 *Pm,
+                              double2 *Am, double2 *Vm, int lane) {
   constexpr int DD = D * D;
-  const int tid = threadIdx.x;
   if (g.kind == 0) {
     double2 *u = A.gates + (long long)s * A.gstride + g.goff;
-    if (tid < 32) {
-      double2 *vs = (A.vstore && D > 2)
-                        ? A.vstore + (long long)s * A.vstride + g.voff + (forward ? DD : 0)
-                        : nullptr;
-      res_update<D>(A, ct, g, u, Uo, Pm, Am, Vm, vs, forward, tid);
-      // operands: backward L = u_old^dagger, R = u_new; forward L = u_new, R = u_old^dagger
-      for (int e = tid; e < DD; e += 32) {
-        const int i = e / D, k = e % D;
-        const double2 od = cconj(Uo[k * D + i]);
-        Ls[e] = forward ? Pm[e] : od;
-        Rs[e] = forward ? od : Pm[e];
-      }
+    double2 *vs = (A.vstore && D > 2)
+                      ? A.vstore + (long long)s * A.vstride + g.voff + (forward ? DD : 0)
+                      : nullptr;
+    res_update<D>(A, ct, g, u, Uo, Pm, Am, Vm, vs, forward, lane);
+    for (int e = lane; e < DD; e += 32) {
+      const int i = e / D, k = e % D;
+      const double2 od = cconj(Uo[k * D + i]);
+      Lb[e] = forward ? Pm[e] : od;
+      Rb[e] = forward ? od : Pm[e];
     }
   } else {
     const double2 *cm = A.cmats + g.goff;
-    for (int e = tid; e < DD; e += blockDim.x) {
+    for (int e = lane; e < DD; e += 32) {
       const int i = e / D, k = e % D;
       const double2 cd = cconj(cm[k * D + i]);
-      Ls[e] = forward ? cm[e] : cd;
-      Rs[e] = forward ? cd : cm[e];
+      Lb[e] = forward ? cm[e] : cd;
+      Rb[e] = forward ? cd : cm[e];
     }
   }
-  __syncthreads();
-  if constexpr (D <= 4)
-    res_sandwich_blocks<D>(ct, g, A.n, A.N, Ls, Rs);
-  else
-    res_sandwich<D>(ct, g, A.n, A.N, Ls, Rs);
+  __syncwarp();
 }
 
-// one gate step dispatched on the gate's arity (only arities <= MAXD exist)
 template <int MAXD>
-__device__ __forceinline__ void res_step_any(const ResidentArgs &A, double2 *ct, const GateDesc &g,
-                                             int s, int forward, double2 *Ls, double2 *Rs,
-                                             double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm) {
+__device__ __forceinline__ void res_prepare(const ResidentArgs &A, const double2 *ct,
+                                            const GateDesc &g, int s, int forward, double2 *Lb,
+                                            double2 *Rb, double2 *Uo, double2 *Pm, double2 *Am,
+                                            double2 *Vm, int lane) {
   if (g.d == 2) {
-    res_step<2>(A, ct, g, s, forward, Ls, Rs, Uo, Pm, Am, Vm);
+    res_prepare_d<2>(A, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      res_step<4>(A, ct, g, s, forward, Ls, Rs, Uo, Pm, Am, Vm);
+      res_prepare_d<4>(A, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
     } else if constexpr (MAXD >= 8) {
-      res_step<8>(A, ct, g, s, forward, Ls, Rs, Uo, Pm, Am, Vm);
+      res_prepare_d<8>(A, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
+    }
+  }
+}
+
+// sandwich of gate g with operands (Lb, Rb); mode/dm/t0/nt as in
+// res_sandwich_blocks.  d = 8 (two-phase, internal barriers) only with mode 0
+// and all threads.
+template <int MAXD>
+__device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResidentArgs &A,
+                                          const double2 *Lb, const double2 *Rb, int mode, int dm,
+                                          int t0, int nt) {
+  if (g.d == 2) {
+    res_sandwich_blocks<2>(ct, g, A.n, A.N, Lb, Rb, mode, dm, t0, nt);
+  } else if constexpr (MAXD >= 4) {
+    if (g.d == 4) {
+      res_sandwich_blocks<4>(ct, g, A.n, A.N, Lb, Rb, mode, dm, t0, nt);
+    } else if constexpr (MAXD >= 8) {
+      res_sandwich<8>(ct, g, A.n, A.N, Lb, Rb);
     }
   }
 }
@@ -288,7 +318,7 @@ template <int MAXD>
 __device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gdesc, int s,
                          double2 *Ls) {
   const int NN = A.N * A.N;
-  for (int e = threadIdx.x; e < NN; e += blockDim.x) ct[e] = A.vdag[e];
+  for (int e = threadIdx.x; e < NN; e += blockDim.x) ct[sidx(e / A.N, e % A.N, A.N)] = A.vdag[e];
   __syncthreads();
   for (int k = 0; k < A.p; k++) {
     const GateDesc &g = gdesc[k];
@@ -317,40 +347,92 @@ __device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gde
   }
 }
 
+// rest-index bits (of gate g) that belong to the location `next_mask`
+__device__ __forceinline__ int rest_bits_in(const GateDesc &g, int n, int next_mask) {
+  int dm = 0;
+#pragma unroll
+  for (int k = 0; k < kMaxQubits; k++)
+    if (k < n - g.m && ((next_mask >> g.rest_pos[k]) & 1)) dm |= 1 << k;
+  return dm;
+}
+
+// Schedule of one TwoSidedSweep as 2p steps: j < p -> (gate p-1-j, backward),
+// j >= p -> (gate j-p, forward).  Step j's operands live in buffer j & 1.
+// Pipelining: step j first applies its sandwich to the blocks that the
+// environment of step j+1 reads (all threads), then warp 0 computes step
+// j+1's update from them while the other warps finish step j's remaining
+// blocks -- the polar factor of the next gate overlaps this gate's
+// sandwich.  Same arithmetic as the sequential order (each block is updated
+// once per step, the next environment reads only final blocks).
 template <int MAXD>
 __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   double2 *ct = reinterpret_cast<double2 *>(smraw);
-  double2 *Ls = ct + A.N * A.N;
-  double2 *Rs = Ls + 64;
-  double2 *Uo = Rs + 64;
+  double2 *Lb = ct + A.N * A.N;  // [2][64]
+  double2 *Rb = Lb + 128;        // [2][64]
+  double2 *Uo = Rb + 128;
   double2 *Pm = Uo + 64;
   double2 *Am = Pm + 64;
   double2 *Vm = Am + 64;
   const GateDesc *gdesc = A.gd;  // global, read through L1
   __shared__ int s_start, s_verdict;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int steps = 2 * A.p;
+  auto gate_of = [&](int j, int &fw) {
+    fw = j >= A.p;
+    return fw ? j - A.p : A.p - 1 - j;
+  };
   for (;;) {
     if (tid == 0) s_start = atomicAdd(A.counter, 1);
     __syncthreads();
     const int s = s_start;
     if (s >= A.S) break;
-    res_init<MAXD>(A, ct, gdesc, s, Ls);
+    res_init<MAXD>(A, ct, gdesc, s, Lb);
     int it = 0;
+    if (A.max_iters > 0) {
+      int fw0;
+      const int k0 = gate_of(0, fw0);
+      if (tid < 32) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, tid);
+      __syncthreads();
+    }
     for (;;) {
       if (A.max_iters > 0) {
-        for (int k = A.p - 1; k >= 0; k--)
-          res_step_any<MAXD>(A, ct, gdesc[k], s, 0, Ls, Rs, Uo, Pm, Am, Vm);
-        for (int k = 0; k < A.p; k++)
-          res_step_any<MAXD>(A, ct, gdesc[k], s, 1, Ls, Rs, Uo, Pm, Am, Vm);
+        for (int j = 0; j < steps; j++) {
+          int fw;
+          const GateDesc &g = gdesc[gate_of(j, fw)];
+          const int buf = (j & 1) * 64, nbuf = 64 - buf;
+          const bool has_next = j + 1 < steps;
+          int fw2 = 0;
+          const int k2 = has_next ? gate_of(j + 1, fw2) : 0;
+          if (A.pipelined && has_next && g.d <= 4 && nt > 32) {
+            const GateDesc &g2 = gdesc[k2];
+            const int dm = rest_bits_in(g, A.n, g2.mask);
+            res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 1, dm, tid, nt);
+            __syncthreads();
+            if (tid < 32)
+              res_prepare<MAXD>(A, ct, g2, s, fw2, Lb + nbuf, Rb + nbuf, Uo, Pm, Am, Vm, tid);
+            else
+              res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 2, dm, tid - 32, nt - 32);
+            __syncthreads();
+          } else {
+            res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 0, 0, tid, nt);
+            __syncthreads();
+            if (has_next) {
+              if (tid < 32)
+                res_prepare<MAXD>(A, ct, gdesc[k2], s, fw2, Lb + nbuf, Rb + nbuf, Uo, Pm, Am, Vm,
+                                  tid);
+              __syncthreads();
+            }
+          }
+        }
         it++;
       }
       // cost + termination, warp 0
       if (tid < 32) {
         double re = 0.0, im = 0.0;
         for (int i = tid; i < A.N; i += 32) {
-          re += ct[i * A.N + i].x;
-          im += ct[i * A.N + i].y;
+          re += ct[sidx(i, i, A.N)].x;
+          im += ct[sidx(i, i, A.N)].y;
         }
         for (int off = 1; off < 32; off <<= 1) {
           re += __shfl_xor_sync(0xffffffffu, re, off);
@@ -399,7 +481,13 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
       }
       __syncthreads();
       if (s_verdict != 0) break;
-      if (it % A.reset_iters == 0) res_init<MAXD>(A, ct, gdesc, s, Ls);
+      if (it % A.reset_iters == 0) res_init<MAXD>(A, ct, gdesc, s, Lb);
+      {  // operands of the next sweep's first step
+        int fw0;
+        const int k0 = gate_of(0, fw0);
+        if (tid < 32) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, tid);
+        __syncthreads();
+      }
     }
     __syncthreads();
   }

@@ -1,0 +1,32 @@
+"""Builds a debug copy of the library with -DQF_POLAR_COUNT and reports the mean
+Newton-Schulz iterations per polar factor on a workload (default C4, 3 sweeps).
+usage: python tools/polar_stats.py [config] [sweeps] [engine]"""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2306_08152_b200 import _build  # noqa: E402
+
+dbg = os.path.join(ROOT, "paper_2306_08152_b200", "libqfactor_debug.so")
+subprocess.check_call([_build.NVCC, *_build.ARCH, *_build.FLAGS, "-DQF_POLAR_COUNT", *_build.sources(),
+                       "-o", dbg])
+_build.LIB = dbg  # load the debug library through the normal binding
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2306_08152_b200 as qf  # noqa: E402
+import qfgen  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C4"
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+eng = {"stream": 1, "resident": 2}.get(sys.argv[3] if len(sys.argv) > 3 else "auto", 0)
+w = qfgen.workload(name)
+c = qf.Circuit.from_workload(w)
+r = qf.qf_instantiate(c, w.target_unitary(), w.initial(), max_iters=iters, engine=eng)
+out = (ctypes.c_ulonglong * 3)()
+qf.lib().qf_debug_polar_counts(out)
+print(f"{name} {iters} sweeps: NS calls {out[0]}, NS iterations {out[1]} "
+      f"({out[1] / max(1, out[0]):.2f} per call), Jacobi sweeps {out[2]}")
