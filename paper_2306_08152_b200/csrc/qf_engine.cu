@@ -875,6 +875,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    if (const char *e = getenv("QF_RES_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
     const int g = std::max(1, std::min(S, std::max(1, per_sm) * E.nsm));
     const int slot = E.prof.on ? E.prof.open(2, st) : -1;
     kern<<<g, threads, smem, st>>>(A);
@@ -1039,5 +1040,8 @@ extern "C" void qf_debug_polar_counts(unsigned long long *out) {
   cudaMemcpyFromSymbol(&out[0], qf::qf_ns_calls, 8);
   cudaMemcpyFromSymbol(&out[1], qf::qf_ns_iters, 8);
   cudaMemcpyFromSymbol(&out[2], qf::qf_polar_sweeps, 8);
+  cudaMemcpyFromSymbol(&out[3], qf::qf_t_serial, 8);
+  cudaMemcpyFromSymbol(&out[4], qf::qf_t_sandwich, 8);
+  cudaMemcpyFromSymbol(&out[5], qf::qf_n_steps, 8);
 }
 #endif

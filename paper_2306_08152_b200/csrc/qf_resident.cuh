@@ -17,6 +17,10 @@
 
 namespace qf {
 
+#ifdef QF_POLAR_COUNT
+__device__ unsigned long long qf_t_serial, qf_t_sandwich, qf_n_steps;
+#endif
+
 struct GateDesc {
   int m, d, kind, goff;   // goff: complex offset in the packed gates (VAR) or in cmats (CONST)
   int mask;               // basis bits of the location
@@ -378,6 +382,11 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
   __shared__ int s_start, s_verdict;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int steps = 2 * A.p;
+  // the serial work (environment, polar factor, cost) runs on warp sw0 (warp 0;
+  // the last warp measured the same)
+  const int sw0 = 0;
+  const bool serial = tid >= sw0;
+  const int lane = tid - sw0;
   auto gate_of = [&](int j, int &fw) {
     fw = j >= A.p;
     return fw ? j - A.p : A.p - 1 - j;
@@ -392,7 +401,7 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
     if (A.max_iters > 0) {
       int fw0;
       const int k0 = gate_of(0, fw0);
-      if (tid < 32) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, tid);
+      if (serial) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, lane);
       __syncthreads();
     }
     for (;;) {
@@ -409,28 +418,41 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
             const int dm = rest_bits_in(g, A.n, g2.mask);
             res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 1, dm, tid, nt);
             __syncthreads();
-            if (tid < 32)
-              res_prepare<MAXD>(A, ct, g2, s, fw2, Lb + nbuf, Rb + nbuf, Uo, Pm, Am, Vm, tid);
+            if (serial)
+              res_prepare<MAXD>(A, ct, g2, s, fw2, Lb + nbuf, Rb + nbuf, Uo, Pm, Am, Vm, lane);
             else
-              res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 2, dm, tid - 32, nt - 32);
+              res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 2, dm, tid, nt - 32);
             __syncthreads();
           } else {
+#ifdef QF_POLAR_COUNT
+            const long long c0 = clock64();
+#endif
             res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 0, 0, tid, nt);
             __syncthreads();
+#ifdef QF_POLAR_COUNT
+            const long long c1 = clock64();
+#endif
             if (has_next) {
-              if (tid < 32)
+              if (serial)
                 res_prepare<MAXD>(A, ct, gdesc[k2], s, fw2, Lb + nbuf, Rb + nbuf, Uo, Pm, Am, Vm,
-                                  tid);
+                                  lane);
               __syncthreads();
             }
+#ifdef QF_POLAR_COUNT
+            if (tid == 0) {
+              atomicAdd(&qf_t_sandwich, (unsigned long long)(c1 - c0));
+              atomicAdd(&qf_t_serial, (unsigned long long)(clock64() - c1));
+              atomicAdd(&qf_n_steps, 1ull);
+            }
+#endif
           }
         }
         it++;
       }
       // cost + termination, warp 0
-      if (tid < 32) {
+      if (serial) {
         double re = 0.0, im = 0.0;
-        for (int i = tid; i < A.N; i += 32) {
+        for (int i = lane; i < A.N; i += 32) {
           re += ct[sidx(i, i, A.N)].x;
           im += ct[sidx(i, i, A.N)].y;
         }
@@ -439,7 +461,7 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
           im += __shfl_xor_sync(0xffffffffu, im, off);
         }
         const double c = 1.0 - hypot(re, im) / (double)A.N;
-        if (tid == 0) {
+        if (lane == 0) {
           int v = 0;
           if (it == 0) {
             v = 4;
@@ -472,10 +494,10 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
         if (A.R > 0 && it >= 1 && it <= A.R) {
           const int slot = A.rec_slot[s];
           if (slot >= 0) {
-            if (tid == 0) A.rec_cost[(long long)slot * A.R + it - 1] = c;
+            if (lane == 0) A.rec_cost[(long long)slot * A.R + it - 1] = c;
             const double *gsrc = reinterpret_cast<const double *>(A.gates + (long long)s * A.gstride);
             double *dst = A.rec_gates + ((long long)slot * A.R + it - 1) * A.var_doubles;
-            for (int e = tid; e < A.var_doubles; e += 32) dst[e] = gsrc[e];
+            for (int e = lane; e < A.var_doubles; e += 32) dst[e] = gsrc[e];
           }
         }
       }
@@ -485,7 +507,7 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
       {  // operands of the next sweep's first step
         int fw0;
         const int k0 = gate_of(0, fw0);
-        if (tid < 32) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, tid);
+        if (serial) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, lane);
         __syncthreads();
       }
     }
