@@ -70,6 +70,8 @@ qf_status check_params(const qf_circuit_s *c, const qf_params *p) {
     return fail(QF_E_ARG, "engine must be QF_ENGINE_AUTO, _STREAM or _RESIDENT");
   if (p->engine == QF_ENGINE_RESIDENT && c->n > 6)
     return fail(QF_E_ARG, "the resident engine holds the tensor in shared memory: n <= 6");
+  if (p->engine == QF_ENGINE_RESIDENT && c->p > 240)
+    return fail(QF_E_ARG, "the resident engine takes at most 240 gates");
   if (p->record_sweeps < 0 || p->record_count < 0)
     return fail(QF_E_ARG, "record_sweeps and record_count must be >= 0");
   if (p->record_count > 0 && p->record_sweeps > 0) {

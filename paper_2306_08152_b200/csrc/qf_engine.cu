@@ -800,7 +800,8 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   }
 
   const bool resident = p.engine == QF_ENGINE_RESIDENT ||
-                        (p.engine == QF_ENGINE_AUTO && c.n <= kResidentMaxQubits);
+                        (p.engine == QF_ENGINE_AUTO && c.n <= kResidentMaxQubits &&
+                         c.p <= kResMaxGates);
   int last = 0;  // last sweep enqueued (streaming engine)
   cudaEvent_t ev[2];
   QF_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -837,7 +838,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.N = N;
     A.p = c.p;
     A.S = S;
-    A.gd = reinterpret_cast<const GateDesc *>(W + E.L.gdesc);
+    for (int k = 0; k < c.p; k++) A.gd[k] = gd[k];
     A.vdag = E.vdag();
     A.cmats = E.cmats();
     A.gates = reinterpret_cast<double2 *>(E.gates());
@@ -846,8 +847,6 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.vstride = E.L.vstride;
     A.counter = counter;
     A.polar_jacobi = E.polar_jacobi ? 1 : 0;
-    A.pipelined = 0;
-    if (const char *e = getenv("QF_PIPELINE")) A.pipelined = std::string(e) == "1";
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;
     A.diff_tol_r = p.diff_tol_r;
@@ -1043,5 +1042,9 @@ extern "C" void qf_debug_polar_counts(unsigned long long *out) {
   cudaMemcpyFromSymbol(&out[3], qf::qf_t_serial, 8);
   cudaMemcpyFromSymbol(&out[4], qf::qf_t_sandwich, 8);
   cudaMemcpyFromSymbol(&out[5], qf::qf_n_steps, 8);
+  cudaMemcpyFromSymbol(&out[6], qf::qf_t_gather, 8);
+  cudaMemcpyFromSymbol(&out[7], qf::qf_t_form, 8);
+  cudaMemcpyFromSymbol(&out[8], qf::qf_t_polar, 8);
+  cudaMemcpyFromSymbol(&out[9], qf::qf_n_upd, 8);
 }
 #endif

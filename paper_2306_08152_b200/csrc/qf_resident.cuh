@@ -19,6 +19,7 @@ namespace qf {
 
 #ifdef QF_POLAR_COUNT
 __device__ unsigned long long qf_t_serial, qf_t_sandwich, qf_n_steps;
+__device__ unsigned long long qf_t_gather, qf_t_form, qf_t_polar, qf_n_upd;
 #endif
 
 struct GateDesc {
@@ -29,9 +30,13 @@ struct GateDesc {
   int rest_pos[kMaxQubits];
 };
 
+// the gate table travels in the kernel parameters (constant bank: uniform,
+// cached loads); templates with more gates use the streaming engine
+constexpr int kResMaxGates = 240;
+
 struct ResidentArgs {
   int n, N, p, S;
-  const GateDesc *gd;
+  GateDesc gd[kResMaxGates];
   const double2 *vdag;
   const double2 *cmats;
   double2 *gates;
@@ -40,7 +45,6 @@ struct ResidentArgs {
   long long vstride;
   int *counter;       // work-stealing start counter (zeroed before launch)
   int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
-  int pipelined;      // 1: overlap the next gate's polar factor with this sandwich
   double dist_tol, diff_tol_a, diff_tol_r, long_diff_r, beta;
   int long_diff_count, min_iters, max_iters, reset_iters, ring;
   double *hist;
@@ -161,57 +165,67 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
   __syncthreads();
 }
 
-// warp 0: environment of gate g from the resident tensor, the update, and the
-// sandwich operands.  Writes u_new to global memory.
+// All threads: environment of gate g from the resident tensor into Pm,
+// P[a][b] = sum_r ct[ins(a,r)][ins(b,r)].  TPO threads of one warp
+// per output take r = k, k+TPO, ... ascending; a fixed xor-tree combines them
+// (deterministic, independent of which CTA runs the start).
 template <int D>
-__device__ void res_update(const ResidentArgs &A, const double2 *ct, const GateDesc &g,
-                           double2 *u, double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm,
-                           double2 *vs, int forward, int lane) {
+__device__ void res_gather_d(const ResidentArgs &A, const double2 *ct, const GateDesc &g,
+                             double2 *Pm) {
   constexpr int DD = D * D;
-  constexpr int SPLIT = DD >= 32 ? 1 : 32 / DD;  // lanes per output
-  constexpr int OPL = DD >= 32 ? DD / 32 : 1;    // outputs per lane
-  const int N = A.N, R = N / D;
-  // global loads first (u_old, the warm-start V): they overlap the gather
-  double2 ureg[OPL], vreg[OPL];
-#pragma unroll
-  for (int q = 0; q < OPL; q++) {
-    const int e = lane + 32 * q;
-    if (e < DD) {
-      ureg[q] = u[e];
-      if (vs) vreg[q] = vs[e];
-    }
-  }
-  // P[a][b] = sum_r ct[ins(a,r)][ins(b,r)]: SPLIT lanes per output take
-  // r = k, k+SPLIT, ... ascending, then a fixed xor-tree combines them
-  const int k = lane % SPLIT;
-#pragma unroll
-  for (int q = 0; q < OPL; q++) {
-    const int o = lane / SPLIT + q * (32 / SPLIT);
-    const int a = o / D, b = o % D;
+  const int nt = blockDim.x, N = A.N, R = N / D;
+  int tpo = nt / DD;  // threads per output: a power of two in [1, 32]
+  tpo = tpo < 1 ? 1 : (tpo > 32 ? 32 : tpo);
+  const int groups = nt / tpo;
+  const int k = threadIdx.x % tpo;
+  for (int o0 = threadIdx.x / tpo; o0 < DD + groups - 1; o0 += groups) {
+    // every lane of a warp runs the same trip count (shuffles below)
+    const int o = o0;
     double2 acc = make_double2(0.0, 0.0);
-    if (o < DD)
-      for (int r = k; r < R; r += SPLIT) {
+    if (o < DD) {
+      const int a = o / D, b = o % D;
+      for (int r = k; r < R; r += tpo) {
         const int sp = rspread(g, A.n, r);
         const double2 v = ct[sidx(sp | g.abits[a], sp | g.abits[b], N)];
         acc.x += v.x;
         acc.y += v.y;
       }
-#pragma unroll
-    for (int off = 1; off < SPLIT; off <<= 1) {
+    }
+    for (int off = 1; off < tpo; off <<= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
     }
     if (k == 0 && o < DD) Pm[o] = acc;
+    if (o0 + groups >= DD) break;
   }
-#pragma unroll
-  for (int q = 0; q < OPL; q++) {
-    const int e = lane + 32 * q;
-    if (e < DD) {
-      Uo[e] = ureg[q];
-      if (vs) Vm[e] = vreg[q];  // warm-start V0, already in place for warp_polar
+}
+
+template <int MAXD>
+__device__ __forceinline__ void res_gather(const ResidentArgs &A, const double2 *ct,
+                                           const GateDesc &g, double2 *Pm) {
+  if (g.d == 2) {
+    res_gather_d<2>(A, ct, g, Pm);
+  } else if constexpr (MAXD >= 4) {
+    if (g.d == 4) {
+      res_gather_d<4>(A, ct, g, Pm);
+    } else if constexpr (MAXD >= 8) {
+      res_gather_d<8>(A, ct, g, Pm);
     }
   }
-  __syncwarp();
+}
+
+// warp 0: the update of gate g from P (Pm) and u_old (Uo), both in shared
+// memory: A = E^dagger (beta), polar factor, u_new to global memory.
+template <int D>
+__device__ void res_update(const ResidentArgs &A, const GateDesc &g, double2 *u, double2 *Uo,
+                           double2 *Pm, double2 *Am, double2 *Vm, double2 *vs, int forward,
+                           int lane) {
+  constexpr int DD = D * D;
+  if (vs)
+    for (int e = lane; e < DD; e += 32) Vm[e] = vs[e];  // warm-start V0 (QF_WARM=1 only)
+#ifdef QF_POLAR_COUNT
+  const long long q1 = clock64();
+#endif
   for (int o = lane; o < DD; o += 32) {
     const int r = o / D, c = o % D;
     double2 acc = make_double2(0.0, 0.0);
@@ -236,7 +250,18 @@ __device__ void res_update(const ResidentArgs &A, const double2 *ct, const GateD
     Am[o] = acc;
   }
   __syncwarp();
+#ifdef QF_POLAR_COUNT
+  const long long q2 = clock64();
+#endif
   warp_polar<D>(Am, Vm, Pm, lane, vs ? Vm : nullptr, A.polar_jacobi != 0);  // u_new -> Pm
+#ifdef QF_POLAR_COUNT
+  if (lane == 0) {
+    const long long q3 = clock64();
+    atomicAdd(&qf_t_form, (unsigned long long)(q2 - q1));
+    atomicAdd(&qf_t_polar, (unsigned long long)(q3 - q2));
+    atomicAdd(&qf_n_upd, 1ull);
+  }
+#endif
   if (vs)
     for (int e = lane; e < DD; e += 32) vs[e] = Vm[e];
   for (int e = lane; e < DD; e += 32) u[e] = Pm[e];
@@ -257,7 +282,7 @@ __device__ void res_prepare_d(const ResidentArgs &A, const double2 *ct, const Ga
     double2 *vs = (A.vstore && D > 2)
                       ? A.vstore + (long long)s * A.vstride + g.voff + (forward ? DD : 0)
                       : nullptr;
-    res_update<D>(A, ct, g, u, Uo, Pm, Am, Vm, vs, forward, lane);
+    res_update<D>(A, g, u, Uo, Pm, Am, Vm, vs, forward, lane);
     for (int e = lane; e < DD; e += 32) {
       const int i = e / D, k = e % D;
       const double2 od = cconj(Uo[k * D + i]);
@@ -362,14 +387,10 @@ __device__ __forceinline__ int rest_bits_in(const GateDesc &g, int n, int next_m
 
 // Schedule of one TwoSidedSweep as 2p steps: j < p -> (gate p-1-j, backward),
 // j >= p -> (gate j-p, forward).  Step j's operands live in buffer j & 1.
-// Pipelining: step j first applies its sandwich to the blocks that the
-// environment of step j+1 reads (all threads), then warp 0 computes step
-// j+1's update from them while the other warps finish step j's remaining
-// blocks -- the polar factor of the next gate overlaps this gate's
-// sandwich.  Same arithmetic as the sequential order (each block is updated
-// once per step, the next environment reads only final blocks).
+// (Overlapping the next gate's polar factor with this sandwich on the other
+// warps was measured slower at 3 CTAs per SM and is not used.)
 template <int MAXD>
-__global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
+__global__ void __launch_bounds__(128) k_resident(const __grid_constant__ ResidentArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   double2 *ct = reinterpret_cast<double2 *>(smraw);
   double2 *Lb = ct + A.N * A.N;  // [2][64]
@@ -378,14 +399,14 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
   double2 *Pm = Uo + 64;
   double2 *Am = Pm + 64;
   double2 *Vm = Am + 64;
-  const GateDesc *gdesc = A.gd;  // global, read through L1
+  const GateDesc *gdesc = A.gd;  // kernel parameters (constant bank)
   __shared__ int s_start, s_verdict;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int steps = 2 * A.p;
   // the serial work (environment, polar factor, cost) runs on warp sw0 (warp 0;
   // the last warp measured the same)
   const int sw0 = 0;
-  const bool serial = tid >= sw0;
+  const bool serial = tid >= sw0 && tid < sw0 + 32;
   const int lane = tid - sw0;
   auto gate_of = [&](int j, int &fw) {
     fw = j >= A.p;
@@ -398,54 +419,66 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
     if (s >= A.S) break;
     res_init<MAXD>(A, ct, gdesc, s, Lb);
     int it = 0;
-    if (A.max_iters > 0) {
-      int fw0;
-      const int k0 = gate_of(0, fw0);
-      if (serial) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, lane);
+    // operands of step j2 into buffer (j2 & 1): all threads gather the
+    // environment (VARIABLE gates), the serial warp stages u_old (prefetched
+    // into registers during the previous sandwich when `pre`), then the serial
+    // warp runs the update
+    double2 upf[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    auto prepare = [&](int j2, bool pre) {
+      int fw2;
+      const GateDesc &g2 = gdesc[gate_of(j2, fw2)];
+      const int off = (j2 & 1) * 64;
+      if (g2.kind == 0) {
+        res_gather<MAXD>(A, ct, g2, Pm);
+        if (serial) {
+          const double2 *u2 = A.gates + (long long)s * A.gstride + g2.goff;
+#pragma unroll
+          for (int q = 0; q < 2; q++) {
+            const int e = lane + 32 * q;
+            if (e < g2.d * g2.d) Uo[e] = pre ? upf[q] : u2[e];
+          }
+        }
+        __syncthreads();
+      }
+      if (serial) res_prepare<MAXD>(A, ct, g2, s, fw2, Lb + off, Rb + off, Uo, Pm, Am, Vm, lane);
       __syncthreads();
-    }
+    };
+    if (A.max_iters > 0) prepare(0, false);
     for (;;) {
       if (A.max_iters > 0) {
         for (int j = 0; j < steps; j++) {
           int fw;
           const GateDesc &g = gdesc[gate_of(j, fw)];
-          const int buf = (j & 1) * 64, nbuf = 64 - buf;
+          const int buf = (j & 1) * 64;
           const bool has_next = j + 1 < steps;
-          int fw2 = 0;
-          const int k2 = has_next ? gate_of(j + 1, fw2) : 0;
-          if (A.pipelined && has_next && g.d <= 4 && nt > 32) {
-            const GateDesc &g2 = gdesc[k2];
-            const int dm = rest_bits_in(g, A.n, g2.mask);
-            res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 1, dm, tid, nt);
-            __syncthreads();
-            if (serial)
-              res_prepare<MAXD>(A, ct, g2, s, fw2, Lb + nbuf, Rb + nbuf, Uo, Pm, Am, Vm, lane);
-            else
-              res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 2, dm, tid, nt - 32);
-            __syncthreads();
-          } else {
-#ifdef QF_POLAR_COUNT
-            const long long c0 = clock64();
-#endif
-            res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 0, 0, tid, nt);
-            __syncthreads();
-#ifdef QF_POLAR_COUNT
-            const long long c1 = clock64();
-#endif
-            if (has_next) {
-              if (serial)
-                res_prepare<MAXD>(A, ct, gdesc[k2], s, fw2, Lb + nbuf, Rb + nbuf, Uo, Pm, Am, Vm,
-                                  lane);
-              __syncthreads();
+          if (has_next && serial) {  // prefetch u_old of the next gate (L2 latency
+            int fw2;                 // hidden behind this sandwich)
+            const GateDesc &g2 = gdesc[gate_of(j + 1, fw2)];
+            if (g2.kind == 0) {
+              const double2 *u2 = A.gates + (long long)s * A.gstride + g2.goff;
+#pragma unroll
+              for (int q = 0; q < 2; q++) {
+                const int e = lane + 32 * q;
+                if (e < g2.d * g2.d) upf[q] = u2[e];
+              }
             }
-#ifdef QF_POLAR_COUNT
-            if (tid == 0) {
-              atomicAdd(&qf_t_sandwich, (unsigned long long)(c1 - c0));
-              atomicAdd(&qf_t_serial, (unsigned long long)(clock64() - c1));
-              atomicAdd(&qf_n_steps, 1ull);
-            }
-#endif
           }
+#ifdef QF_POLAR_COUNT
+          const long long c0 = clock64();
+#endif
+          res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 0, 0, tid, nt);
+          __syncthreads();
+#ifdef QF_POLAR_COUNT
+          const long long c1 = clock64();
+#endif
+          if (has_next) prepare(j + 1, true);
+#ifdef QF_POLAR_COUNT
+          if (tid == 0) {
+            atomicAdd(&qf_t_sandwich, (unsigned long long)(c1 - c0));
+            atomicAdd(&qf_t_serial, (unsigned long long)(clock64() - c1));
+            atomicAdd(&qf_n_steps, 1ull);
+          }
+#endif
         }
         it++;
       }
@@ -504,12 +537,7 @@ __global__ void __launch_bounds__(128) k_resident(const ResidentArgs A) {
       __syncthreads();
       if (s_verdict != 0) break;
       if (it % A.reset_iters == 0) res_init<MAXD>(A, ct, gdesc, s, Lb);
-      {  // operands of the next sweep's first step
-        int fw0;
-        const int k0 = gate_of(0, fw0);
-        if (serial) res_prepare<MAXD>(A, ct, gdesc[k0], s, fw0, Lb, Rb, Uo, Pm, Am, Vm, lane);
-        __syncthreads();
-      }
+      prepare(0, false);  // operands of the next sweep's first step
     }
     __syncthreads();
   }

@@ -26,10 +26,13 @@ eng = {"stream": 1, "resident": 2}.get(sys.argv[3] if len(sys.argv) > 3 else "au
 w = qfgen.workload(name)
 c = qf.Circuit.from_workload(w)
 r = qf.qf_instantiate(c, w.target_unitary(), w.initial(), max_iters=iters, engine=eng)
-out = (ctypes.c_ulonglong * 6)()
+out = (ctypes.c_ulonglong * 10)()
 qf.lib().qf_debug_polar_counts(out)
 print(f"{name} {iters} sweeps: NS calls {out[0]}, NS iterations {out[1]} "
       f"({out[1] / max(1, out[0]):.2f} per call), Jacobi sweeps {out[2]}")
 if out[5]:
     print(f"  resident: per step serial {out[3] / out[5]:.0f} cycles, sandwich {out[4] / out[5]:.0f} "
           f"cycles ({out[5]} steps)")
+if out[9]:
+    print(f"  update: u_old load + gather {out[6] / out[9]:.0f}, form A {out[7] / out[9]:.0f}, "
+          f"polar {out[8] / out[9]:.0f} cycles")
