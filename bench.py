@@ -206,7 +206,7 @@ def roofline(st, step_ms, w):
                 "alg_flops_per_launch": flops / len(st), "launches": len(st),
                 "avg_launch_us": 1e3 * t_ms / len(st), "share_of_step": t_ms / step_ms,
                 "peak_source": src,
-                "flops_def": "16*d*N^2 per gate step + 8*d*N^2 per init pass (complex fp64 FMA = 8 flop)"}
+                "flops_def": "16*d*N^2 per two-sided gate step (2 per gate per sweep) + 8*d*N^2 per one-sided init pass (complex fp64 FMA = 8 flop)"}
     sw_bytes = sum(s["sandwich_bytes"] for s in st)
     sw_ms = sum(s["sandwich_ms"] for s in st)
     sw_n = sum(s["sandwich_launches"] for s in st)

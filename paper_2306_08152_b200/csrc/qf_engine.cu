@@ -471,24 +471,35 @@ struct Engine {
   // fused partials available for env(part_k, part_dir) / the trace
   int part_k = -1, part_dir = 0, part_tiles = 0, tpart_tiles = 0;
 
-  template <int D>
-  cudaError_t launch_reg(const SandwichArgs &A) {
-    int &grid = reg_grid[ilog2(D)];
+  template <int D, int NT, int MINB>
+  cudaError_t launch_reg_v(const SandwichArgs &A, int &grid) {
     if (grid == 0) {
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sandwich_reg<D>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sandwich_reg<D, NT, MINB>, NT, 0);
       grid = std::max(1, per_sm) * nsm;
     }
     const int NR = N / D;
-    const long long total = (long long)S * ((NR * NR + 255) / 256);
+    const long long total = (long long)S * ((NR * NR + NT - 1) / NT);
     const int g = (int)std::max<long long>(1, std::min<long long>(grid, total));
     const int slot = prof.on ? prof.open(0, st) : -1;
-    k_sandwich_reg<D><<<g, 256, 0, st>>>(A);
+    k_sandwich_reg<D, NT, MINB><<<g, NT, 0, st>>>(A);
     if (slot >= 0) prof.close(slot, st);
     launches++;
     sw_ctx[ctx]++;
     return cudaGetLastError();
   }
+  template <int D>
+  cudaError_t launch_reg(const SandwichArgs &A) {
+    int &grid = reg_grid[ilog2(D)];
+    switch (reg_variant) {
+      case 1: return launch_reg_v<D, 256, 2>(A, grid);
+      case 2: return launch_reg_v<D, 128, 3>(A, grid);
+      case 3: return launch_reg_v<D, 128, 4>(A, grid);
+      case 4: return launch_reg_v<D, 64, 6>(A, grid);
+      default: return launch_reg_v<D, 256, 1>(A, grid);
+    }
+  }
+  int reg_variant = getenv("QF_REG") ? atoi(getenv("QF_REG")) : 2;
   int reg_grid[4] = {0, 0, 0, 0};
 
   cudaError_t sandwich(const SandwichArgs &A) {
@@ -996,8 +1007,8 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     r.stats.resident_ms = E.prof.ms[2];
     {
       double step_f = 0.0, init_f = 0.0;
-      for (int k = 0; k < c.p; k++) {
-        step_f += 16.0 * (1 << c.arity[k]) * (double)N * N;
+      for (int k = 0; k < c.p; k++) {  // a sweep = 2 two-sided steps per gate
+        step_f += 2.0 * 16.0 * (1 << c.arity[k]) * (double)N * N;
         init_f += 8.0 * (1 << c.arity[k]) * (double)N * N;
       }
       double f = 0.0, passes = 0.0;

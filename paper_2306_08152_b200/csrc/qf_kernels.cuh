@@ -1100,13 +1100,14 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
 // staging of the tensor and no barriers in the steady state; lanes run over
 // consecutive c so every load/store instruction of a warp covers 32
 // consecutive elements when the location's bits are not the lowest ones.
-// A CTA handles 256 consecutive blocks of one start per chunk.
-template <int D>
-__global__ void __launch_bounds__(256) k_sandwich_reg(const SandwichArgs A) {
+// A CTA handles NT consecutive blocks of one start per chunk; element
+// indices are 32-bit (N^2 <= 2^24 for n <= kMaxQubits).
+template <int D, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_sandwich_reg(const SandwichArgs A) {
   __shared__ double2 Ls[D * D], Rs[D * D];
   const int N = A.N, NR = N / D;
   const int bps = NR * NR;                      // blocks per start
-  const int cps = (bps + 255) / 256;            // chunks per start
+  const int cps = (bps + NT - 1) / NT;          // chunks per start
   const int nact = *A.n_active;
   const long long total = (long long)nact * cps;
   const long long per = (total + gridDim.x - 1) / gridDim.x;
@@ -1132,17 +1133,16 @@ __global__ void __launch_bounds__(256) k_sandwich_reg(const SandwichArgs A) {
       cur = s;
       __syncthreads();
     }
-    const int bi = (int)(ch - (long long)ai * cps) * 256 + tid;
+    const int bi = (int)(ch - (long long)ai * cps) * NT + tid;
     if (bi >= bps) continue;
     const int r = bi / NR, c = bi - (bi / NR) * NR;
-    const int rb = spread_rest(A.b, r), cb = spread_rest(A.b, c);
+    const int base = spread_rest(A.b, r) * N + spread_rest(A.b, c);
     double2 *cts = A.ct + (long long)s * A.ct_stride;
     double2 x[D][D];
 #pragma unroll
     for (int a = 0; a < D; a++)
 #pragma unroll
-      for (int b = 0; b < D; b++)
-        x[a][b] = cts[(long long)(rb | A.b.abits[a]) * N + (cb | A.b.abits[b])];
+      for (int b = 0; b < D; b++) x[a][b] = cts[base + A.b.abits[a] * N + A.b.abits[b]];
     // left: column by column, in place in registers
 #pragma unroll
     for (int b = 0; b < D; b++) {
@@ -1160,7 +1160,7 @@ __global__ void __launch_bounds__(256) k_sandwich_reg(const SandwichArgs A) {
     // right: row by row, straight to global memory
 #pragma unroll
     for (int a = 0; a < D; a++) {
-      double2 *row = cts + (long long)(rb | A.b.abits[a]) * N + cb;
+      double2 *row = cts + base + A.b.abits[a] * N;
       if (has_r) {
 #pragma unroll
         for (int b = 0; b < D; b++) {

@@ -74,10 +74,23 @@ def haar(keys, d):
     r = np.sqrt(-2.0 * np.log(u1))
     z = (r * np.cos(2 * np.pi * u2) + 1j * r * np.sin(2 * np.pi * u2)) / np.sqrt(2.0)
     z = z.reshape(-1, d, d)
-    q, rr = np.linalg.qr(z)
-    ph = np.diagonal(rr, axis1=1, axis2=2)
-    ph = ph / np.abs(ph)
-    return q * ph[:, None, :]
+    # Q of the QR factorisation with a positive real diagonal of R ("phase
+    # fix", Mezzadri 2007), by twice-iterated modified Gram-Schmidt vectorised
+    # over the batch (the same unique Q as LAPACK QR + phase fix, much faster
+    # for millions of small matrices); columns laid out batch-contiguous and
+    # processed in cache-sized chunks
+    q = np.empty_like(z)
+    for c0 in range(0, z.shape[0], 16384):
+        zt = np.ascontiguousarray(z[c0:c0 + 16384].transpose(2, 1, 0))  # [col][row][batch]
+        qt = np.empty_like(zt)
+        for j in range(d):
+            v = zt[j].copy()
+            for _ in range(2):
+                for i in range(j):
+                    v -= np.sum(np.conj(qt[i]) * v, axis=0) * qt[i]
+            qt[j] = v / np.sqrt(np.sum(v.real ** 2 + v.imag ** 2, axis=0))
+        q[c0:c0 + 16384] = qt.transpose(2, 1, 0)
+    return q
 
 
 @dataclass
