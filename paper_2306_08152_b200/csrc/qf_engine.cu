@@ -426,7 +426,22 @@ struct Engine {
     A.tiles_per_start = rt.second;
     const size_t tile_bytes = (size_t)A.RT * D * N * 16;
     A.stages = (int)std::max<size_t>(2, std::min<size_t>(4, (96 * 1024) / tile_bytes));
-    const size_t smem = A.stages * tile_bytes + 2 * D * D * 16 + 2 * A.stages * 8 + 2 * kMaxTileRows * 4;
+    const size_t smem = A.stages * tile_bytes + 2 * D * D * 16 + 2 * A.stages * 8 + 2 * kMaxTileRows * 4 + 16 * 4;
+    {
+      // bank spreading of phase 2: the gate's bits among basis positions
+      // {0,1,2} (g of them, local index bits gl[]) are driven by the upper g
+      // of the 3 low bits of c, whose lower 3-g bits already select the bank
+      int gl[3], g = 0;
+      for (int pos = 0; pos < 3; pos++)
+        for (int i = 0; i < A.b.m; i++)
+          if (A.b.abits[1 << i] == (1 << pos)) gl[g++] = i;
+      for (int q = 0; q < 8; q++) {
+        int r = 0;
+        for (int t = 0; t < g; t++)
+          if ((q >> (3 - g + t)) & 1) r |= 1 << gl[t];
+        A.rot[q] = r & (D - 1);
+      }
+    }
     // fused epilogue for the next step
     if (next_k >= 0) {
       const Bits nb = make_bits(c, next_k);

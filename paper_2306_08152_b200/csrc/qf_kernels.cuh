@@ -890,6 +890,11 @@ struct RowTileArgs {
   int RT;               // row-rests per tile
   int tiles_per_start;  // (N/d)/RT
   int stages;           // ring depth
+  // phase-2 bank spreading: item c runs over the gate's local column index
+  // in the order b ^ rot[c & 7] (a permutation of 0..d-1), so that the 8
+  // lanes of a quarter-warp hit 8 different shared-memory banks even when
+  // the gate owns low basis bits (see launch_rows)
+  int rot[8];
   // fused epilogue for the NEXT step of the schedule (reads the finished tile
   // in shared memory): partial environment of the next VARIABLE gate,
   //   part[s][tile][a'*d'+b'] = sum_{tile rows i, i&nmask == nab[a']}
@@ -926,7 +931,12 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
   uint64_t *full = reinterpret_cast<uint64_t *>(Rs + D * D);
   uint64_t *computed = full + A.stages;
   int *rid_buf = reinterpret_cast<int *>(computed + A.stages);  // 2 x kMaxTileRows
+  int *sab = rid_buf + 2 * kMaxTileRows;                         // abits[8], rot[8]
   const int tid = threadIdx.x;
+  if (tid < 8) {
+    sab[tid] = A.b.abits[tid];
+    sab[8 + tid] = A.rot[tid];
+  }
   const bool has_r = A.rsrc != nullptr;
 
   const int nact = *A.n_active;
@@ -1039,21 +1049,24 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
     }
     if (has_r) {
       csync();
-      // phase 2: right multiply, d columns ins(b, c) of one row per item
+      // phase 2: right multiply, d columns ins(b, c) of one row per item,
+      // local column order permuted by m = rot[c & 7] (R's indices follow)
       for (int it = tid; it < A.RT * N; it += kRowThreads) {
         const int rl = it / N, rem = it - rl * N;
         const int a = rem / NC, c = rem - a * NC;
         double2 *row = tile + (size_t)(rl * D + a) * N;
         const int cb = spread_rest(A.b, c);
+        const int m = sab[8 + (c & 7)];
         double2 z[D];
 #pragma unroll
-        for (int b = 0; b < D; b++) z[b] = row[cb | A.b.abits[b]];
+        for (int j = 0; j < D; j++) z[j] = row[cb | sab[j ^ m]];
 #pragma unroll
         for (int b = 0; b < D; b++) {
+          const int bt = b ^ m;
           double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-          for (int k = 0; k < D; k++) acc = cfma(z[k], Rs[k * D + b], acc);
-          row[cb | A.b.abits[b]] = acc;
+          for (int j = 0; j < D; j++) acc = cfma(z[j], Rs[(j ^ m) * D + bt], acc);
+          row[cb | sab[bt]] = acc;
         }
       }
     }
