@@ -70,11 +70,7 @@ __device__ __forceinline__ int swz(int j) {
 __device__ __forceinline__ int sidx(int i, int j, int N) { return i * N + swz(j); }
 
 __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
-  int x = 0;
-#pragma unroll
-  for (int k = 0; k < kMaxQubits; k++)
-    if (k < n - g.m) x |= ((r >> k) & 1) << g.rest_pos[k];
-  return x;
+  return insert_zeros(r, g.mask);
 }
 
 // ct <- E(L) ct E(R) in place for D <= 4, one D x D block (row-rest r,
@@ -429,7 +425,13 @@ __global__ void __launch_bounds__(128) k_resident(const __grid_constant__ Reside
       const GateDesc &g2 = gdesc[gate_of(j2, fw2)];
       const int off = (j2 & 1) * 64;
       if (g2.kind == 0) {
+#ifdef QF_POLAR_COUNT
+        const long long tg0 = clock64();
+#endif
         res_gather<MAXD>(A, ct, g2, Pm);
+#ifdef QF_POLAR_COUNT
+        if (tid == 0) atomicAdd(&qf_t_gather, (unsigned long long)(clock64() - tg0));
+#endif
         if (serial) {
           const double2 *u2 = A.gates + (long long)s * A.gstride + g2.goff;
 #pragma unroll

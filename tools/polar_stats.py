@@ -34,5 +34,5 @@ if out[5]:
     print(f"  resident: per step serial {out[3] / out[5]:.0f} cycles, sandwich {out[4] / out[5]:.0f} "
           f"cycles ({out[5]} steps)")
 if out[9]:
-    print(f"  update: u_old load + gather {out[6] / out[9]:.0f}, form A {out[7] / out[9]:.0f}, "
+    print(f"  gather (all threads, before the barrier) {out[6] / out[9]:.0f}, form A {out[7] / out[9]:.0f}, "
           f"polar {out[8] / out[9]:.0f} cycles")
