@@ -517,43 +517,34 @@ __device__ __forceinline__ void warp_mm(const double2 *Am, const double2 *Bm, do
 }
 
 // Unitary polar factor by the quintic Newton-Schulz iteration
-//   X <- X (15 I - 10 Y + 3 Y^2) / 8,   Y = X^H X,   X_0 = A / ||A||_F,
-// which keeps the singular vectors of A and drives every singular value in
-// (0, 1] to 1 (growth 15/8 per step while small, cubic convergence near 1).
-// Every step is three small matrix products done by all lanes at once, so its
-// latency is a few hundred cycles against ~1000 per Jacobi round.  Stops one
-// step after max |Y - I| <= 1e-5 (error then ~(1e-5)^3).  Returns false if it
-// has not converged after 48 steps (A singular or near it); X (in Am) then
-// still has the polar factor of A and the caller finishes with Jacobi.
+//   X <- X (15 I - 10 Y + 3 Y^2) / 8,   Y = X^H X,   X_0 = A / sqrt(g),
+// g >= sigma_max(A)^2 the largest absolute row sum of A^H A (Gershgorin), so
+// every singular value of X_0 is in (0, 1]; the iteration keeps the singular
+// vectors of A and drives the singular values to 1 (cubic convergence near
+// 1).  While some |Y - I| entry exceeds 0.55 (at most 8 steps) it takes the
+// steeper quintic p(s) = 3.4445 s - 4.7750 s^3 + 2.0315 s^5 (maps (0, 1.2]
+// into (0, 1.2], slope 3.44 at 0) instead.  Stops one step after
+// max |Y - I| <= 1e-5 (error then ~(1e-5)^3).  Returns false if A is zero or
+// not finite, or has not converged after 48 steps (A singular or near it);
+// Xm then holds A or an iterate with the same polar factor and the caller
+// finishes with Jacobi.
 // Buffers: X in Xm (in place), Y in Ym, W in Wm; result copied to U (may
-// alias Wm).  Each lane keeps its output entries of X and Y in registers
-// (for D = 4 lanes 16..31 mirror lanes 0..15, so every lane does the same
-// work and no branch diverges), which saves the shared-memory round trips of
-// forming W and of the convergence test (1.7x lower latency than staging
-// every product in shared memory, bitwise the same result).
+// alias Wm).  Each lane keeps its output entries of X and Y in registers (for
+// D = 4 lanes 16..31 mirror lanes 0..15, so every lane does the same work and
+// no branch diverges) and both tests share one warp reduction: 0.55x the
+// latency of staging every product in shared memory (tools/ns_bench.cu).
 template <int D>
 __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U, int lane) {
   constexpr int DD = D * D, OPL = (DD + 31) / 32;
   int oo[OPL];
   bool wr[OPL];
   double2 x[OPL], y[OPL];
-  double f = 0.0;
 #pragma unroll
   for (int q = 0; q < OPL; q++) {
     oo[q] = (lane + 32 * q) & (DD - 1);
     wr[q] = lane + 32 * q < DD;
     x[q] = Xm[oo[q]];
-    if (wr[q]) f += cabs2(x[q]);
   }
-  for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
-  if (!(f > 0.0) || !isfinite(f)) return false;
-  const double sc = rsqrt(f);
-#pragma unroll
-  for (int q = 0; q < OPL; q++) {
-    x[q] = cscale(x[q], sc);
-    if (wr[q]) Xm[oo[q]] = x[q];
-  }
-  __syncwarp();
   bool done = false, fast = true;
 #ifdef QF_POLAR_COUNT
   if (lane == 0) atomicAdd(&qf_ns_calls, 1ull);
@@ -584,6 +575,7 @@ __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U,
         for (int k = 0; k < D; k++) rs += fabs(Ym[lane * D + k].x) + fabs(Ym[lane * D + k].y);
       }
       const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(rs) >> 32));
+      if (hi == 0u || hi >= 0x7ff00000u) return false;  // A = 0, or Inf / NaN entries
       const double gmax = __longlong_as_double((long long)(hi + 1u) << 32);
       const double s1 = rsqrt(gmax * (1.0 + 1e-5)), s2 = s1 * s1;
 #pragma unroll
@@ -596,16 +588,19 @@ __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U,
       for (int q = 0; q < OPL; q++)
         if (wr[q]) Xm[oo[q]] = x[q];
     }
-    double dev = 0.0;
+    // one reduction for both tests: 2 = some |Y - I| entry > 0.55 (or NaN),
+    // 1 = some > 1e-5, 0 = converged
+    unsigned code = 0;
 #pragma unroll
     for (int q = 0; q < OPL; q++) {
       if (wr[q]) Ym[oo[q]] = y[q];
-      const double dx = y[q].x - (oo[q] / D == oo[q] % D ? 1.0 : 0.0);
-      dev = fmax(dev, fmax(fabs(dx), fabs(y[q].y)));
-      if (!(dx == dx && y[q].y == y[q].y)) dev = INFINITY;
+      const double ax = fabs(y[q].x - (oo[q] / D == oo[q] % D ? 1.0 : 0.0)), ay = fabs(y[q].y);
+      const unsigned cq = !(ax <= 0.55 && ay <= 0.55) ? 2u : (!(ax <= 1e-5 && ay <= 1e-5) ? 1u : 0u);
+      code = cq > code ? cq : code;
     }
-    done = !__any_sync(0xffffffffu, !(dev <= 1e-5));
-    if (fast) fast = it < 8 && __any_sync(0xffffffffu, !(dev <= 0.55));
+    code = __reduce_max_sync(0xffffffffu, code);
+    done = code == 0;
+    if (fast) fast = it < 8 && code == 2;
     const double ca = fast ? 3.4445 : 1.875, cb = fast ? -4.7750 : -1.25,
                  cc = fast ? 2.0315 : 0.375;
     __syncwarp();

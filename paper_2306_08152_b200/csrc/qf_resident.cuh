@@ -83,9 +83,10 @@ template <int D>
 __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N,
                                     const double2 *Ls, const double2 *Rs, int mode, int dm,
                                     int t0, int nt) {
-  const int NR = N / D;
+  constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
+  const int lnr = n - LD, NR = 1 << lnr;  // N / D rests (no runtime division)
   for (int it = t0; it < NR * NR; it += nt) {
-    const int r = it / NR, c = it - r * NR;
+    const int r = it >> lnr, c = it & (NR - 1);
     if (mode != 0 && (((r ^ c) & ~dm) == 0) != (mode == 1)) continue;
     const int rb = rspread(g, n, r), cb = rspread(g, n, c);
     double2 x[D][D];
@@ -120,11 +121,12 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
 template <int D>
 __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const double2 *Ls,
                              const double2 *Rs) {
-  const int NR = N / D;  // rests
+  constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
+  const int lnr = n - LD, NR = 1 << lnr;  // rests
   const int nt = blockDim.x;
   // phase 1: item (row-rest r, column j) mixes the D rows ins(a, r) of column j
   for (int it = threadIdx.x; it < NR * N; it += nt) {
-    const int r = it / N, j = it - r * N;
+    const int r = it >> n, j = it & (N - 1);
     const int rb = rspread(g, n, r);
     double2 x[D];
 #pragma unroll
@@ -144,7 +146,7 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
   __syncthreads();
   // phase 2: item (row i, column-rest c) mixes the D columns ins(b, c) of row i
   for (int it = threadIdx.x; it < N * NR; it += nt) {
-    const int i = it / NR, c = it - i * NR;
+    const int i = it >> lnr, c = it & (NR - 1);
     const int cb = rspread(g, n, c);
     double2 *row = ct + i * N;
     double2 z[D];
@@ -169,12 +171,15 @@ template <int D>
 __device__ void res_gather_d(const ResidentArgs &A, const double2 *ct, const GateDesc &g,
                              double2 *Pm) {
   constexpr int DD = D * D;
-  const int nt = blockDim.x, N = A.N, R = N / D;
-  int tpo = nt / DD;  // threads per output: a power of two in [1, 32]
-  tpo = tpo < 1 ? 1 : (tpo > 32 ? 32 : tpo);
-  const int groups = nt / tpo;
-  const int k = threadIdx.x % tpo;
-  for (int o0 = threadIdx.x / tpo; o0 < DD + groups - 1; o0 += groups) {
+  constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
+  const int nt = blockDim.x, N = A.N, R = N >> LD;
+  // threads per output: a power of two in [1, 32] (shifts, no runtime division)
+  int ltpo = (31 - __clz(nt)) - 2 * LD;
+  ltpo = ltpo < 0 ? 0 : (ltpo > 5 ? 5 : ltpo);
+  const int tpo = 1 << ltpo;
+  const int groups = nt >> ltpo;
+  const int k = threadIdx.x & (tpo - 1);
+  for (int o0 = threadIdx.x >> ltpo; o0 < DD + groups - 1; o0 += groups) {
     // every lane of a warp runs the same trip count (shuffles below)
     const int o = o0;
     double2 acc = make_double2(0.0, 0.0);
@@ -343,7 +348,8 @@ template <int MAXD>
 __device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gdesc, int s,
                          double2 *Ls) {
   const int NN = A.N * A.N;
-  for (int e = threadIdx.x; e < NN; e += blockDim.x) ct[sidx(e / A.N, e % A.N, A.N)] = A.vdag[e];
+  for (int e = threadIdx.x; e < NN; e += blockDim.x)
+    ct[sidx(e >> A.n, e & (A.N - 1), A.N)] = A.vdag[e];
   __syncthreads();
   for (int k = 0; k < A.p; k++) {
     const GateDesc &g = gdesc[k];
