@@ -94,7 +94,10 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
     for (int a = 0; a < D; a++)
 #pragma unroll
       for (int b = 0; b < D; b++) x[a][b] = ct[sidx(rb | g.abits[a], cb | g.abits[b], N)];
-    // row by row: z[a][:] = (L[a][:] x) R, stored over the (register-held) block
+    // row by row: z[a][:] = (L[a][:] x) R, stored over the (register-held)
+    // block.  The outputs go in pairs: a store may alias the next R loads
+    // for the compiler, so a pair gives it four independent accumulation
+    // chains to interleave instead of two
 #pragma unroll
     for (int a = 0; a < D; a++) {
       double2 y[D];
@@ -107,11 +110,15 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
         for (int b = 0; b < D; b++) y[b] = cfma(l, x[k][b], y[b]);
       }
 #pragma unroll
-      for (int b = 0; b < D; b++) {
-        double2 z = make_double2(0.0, 0.0);
+      for (int b = 0; b < D; b += 2) {
+        double2 z0 = make_double2(0.0, 0.0), z1 = z0;
 #pragma unroll
-        for (int k = 0; k < D; k++) z = cfma(y[k], Rs[k * D + b], z);
-        ct[sidx(rb | g.abits[a], cb | g.abits[b], N)] = z;
+        for (int k = 0; k < D; k++) {
+          z0 = cfma(y[k], Rs[k * D + b], z0);
+          z1 = cfma(y[k], Rs[k * D + b + 1], z1);
+        }
+        ct[sidx(rb | g.abits[a], cb | g.abits[b], N)] = z0;
+        ct[sidx(rb | g.abits[a], cb | g.abits[b + 1], N)] = z1;
       }
     }
   }
@@ -392,7 +399,7 @@ __device__ __forceinline__ int rest_bits_in(const GateDesc &g, int n, int next_m
 // (Overlapping the next gate's polar factor with this sandwich on the other
 // warps was measured slower at 3 CTAs per SM and is not used.)
 template <int MAXD>
-__global__ void __launch_bounds__(128) k_resident(const __grid_constant__ ResidentArgs A) {
+__global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ ResidentArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   double2 *ct = reinterpret_cast<double2 *>(smraw);
   double2 *Lb = ct + A.N * A.N;  // [2][64]
