@@ -873,6 +873,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.vstride = E.L.vstride;
     A.counter = counter;
     A.polar_jacobi = E.polar_jacobi ? 1 : 0;
+    A.gather_ltpo_max = getenv("QF_GATHER_LTPO") ? std::max(0, std::min(5, atoi(getenv("QF_GATHER_LTPO")))) : 5;
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;
     A.diff_tol_r = p.diff_tol_r;

@@ -45,6 +45,7 @@ struct ResidentArgs {
   long long vstride;
   int *counter;       // work-stealing start counter (zeroed before launch)
   int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
+  int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   double dist_tol, diff_tol_a, diff_tol_r, long_diff_r, beta;
   int long_diff_count, min_iters, max_iters, reset_iters, ring;
   double *hist;
@@ -182,7 +183,7 @@ __device__ void res_gather_d(const ResidentArgs &A, const double2 *ct, const Gat
   const int nt = blockDim.x, N = A.N, R = N >> LD;
   // threads per output: a power of two in [1, 32] (shifts, no runtime division)
   int ltpo = (31 - __clz(nt)) - 2 * LD;
-  ltpo = ltpo < 0 ? 0 : (ltpo > 5 ? 5 : ltpo);
+  ltpo = ltpo < 0 ? 0 : (ltpo > A.gather_ltpo_max ? A.gather_ltpo_max : ltpo);
   const int tpo = 1 << ltpo;
   const int groups = nt >> ltpo;
   const int k = threadIdx.x & (tpo - 1);
