@@ -5,7 +5,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -22,6 +26,76 @@ void set_error(const std::string &msg) { g_err = msg; }
 qf_status cuda_fail(cudaError_t e, const char *what) {
   set_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
   return QF_E_CUDA;
+}
+
+// ---- pinned host pool (qf_internal.h).  Buffers are never returned to the
+// driver at exit (the context may already be gone); the cache is bounded.
+namespace {
+constexpr size_t kPinnedCacheBytes = size_t(4) << 30;
+std::mutex g_pin_mu;
+std::multimap<size_t, void *> g_pin_free;  // capacity -> buffer
+size_t g_pin_cached = 0;
+}  // namespace
+
+void *pinned_get(size_t bytes, size_t *cap, bool *pinned) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+      void *p = it->second;
+      *cap = it->first;
+      *pinned = true;
+      g_pin_cached -= it->first;
+      g_pin_free.erase(it);
+      return p;
+    }
+  }
+  void *p = nullptr;
+  if (cudaMallocHost(&p, bytes) == cudaSuccess) {
+    *cap = bytes;
+    *pinned = true;
+    return p;
+  }
+  cudaGetLastError();  // clear the sticky-free error of a failed pin
+  p = std::malloc(bytes);
+  *cap = p ? bytes : 0;
+  *pinned = false;
+  return p;
+}
+
+void pinned_put(void *p, size_t cap, bool pinned) {
+  if (!pinned) {
+    std::free(p);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  while (g_pin_cached + cap > kPinnedCacheBytes && !g_pin_free.empty()) {
+    auto it = g_pin_free.begin();  // drop the smallest cached buffers first
+    cudaFreeHost(it->second);
+    g_pin_cached -= it->first;
+    g_pin_free.erase(it);
+  }
+  if (g_pin_cached + cap > kPinnedCacheBytes) {
+    cudaFreeHost(p);
+    return;
+  }
+  g_pin_free.emplace(cap, p);
+  g_pin_cached += cap;
+}
+
+// keep freed stream-ordered allocations in the device's default pool between
+// calls (the default release threshold of 0 unmaps them at every synchronize)
+void retain_device_pool() {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
 }
 
 }  // namespace qf
@@ -239,6 +313,7 @@ qf_status qf_instantiate(qf_circuit_t c, const double *target, const double *ini
   const size_t N = (size_t)1 << c->n;
   const size_t tbytes = N * N * 16, ibytes = (size_t)p->num_starts * c->var_doubles * 8;
   const size_t wbytes = qf::engine_workspace_size(*c, *p);
+  qf::retain_device_pool();
   cudaStream_t st = nullptr;
   if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
     return qf::cuda_fail(e, "cudaStreamCreate");

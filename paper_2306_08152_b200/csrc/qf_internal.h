@@ -9,6 +9,48 @@
 
 #include "qf.h"
 
+namespace qf {
+
+// Page-locked host memory recycled across calls: result arrays of the host
+// entry point are filled by device->host copies at full link speed, and the
+// pinning cost (~ms per 100 MB) is paid once per size class, not per call.
+// Thread-safe; keeps at most kPinnedCacheBytes of freed buffers.
+void *pinned_get(size_t bytes, size_t *cap, bool *pinned);
+void pinned_put(void *p, size_t cap, bool pinned);
+
+// Uninitialised double array in pooled pinned memory (falls back to
+// pageable memory if pinning fails).
+class HostArray {
+ public:
+  HostArray() = default;
+  HostArray(const HostArray &) = delete;
+  HostArray &operator=(const HostArray &) = delete;
+  ~HostArray() { release(); }
+  void resize(size_t n) {
+    if (n * 8 > cap_) {
+      release();
+      p_ = static_cast<double *>(pinned_get(n * 8, &cap_, &pinned_));
+    }
+    n_ = p_ ? n : 0;
+  }
+  double *data() { return p_; }
+  const double *data() const { return p_; }
+  size_t size() const { return n_; }
+  bool empty() const { return n_ == 0; }
+
+ private:
+  void release() {
+    if (p_) pinned_put(p_, cap_, pinned_);
+    p_ = nullptr;
+    n_ = cap_ = 0;
+  }
+  double *p_ = nullptr;
+  size_t n_ = 0, cap_ = 0;
+  bool pinned_ = false;
+};
+
+}  // namespace qf
+
 struct qf_circuit_s {
   int n = 0, p = 0;
   std::vector<int> arity;      // p
@@ -26,7 +68,7 @@ struct qf_result_s {
   int var_doubles = 0;
   int best = -1;
   std::vector<qf_summary> summary;   // S
-  std::vector<double> gates;         // S x var (host call) or 1 x var (best only)
+  qf::HostArray gates;               // S x var (host call) or 1 x var (best only)
   bool all_gates = false;
   int record_sweeps = 0, record_count = 0;
   std::vector<double> rec_cost;      // record_count x R
