@@ -63,8 +63,32 @@ typedef enum {
   QF_PLATEAU_SHORT = 2, /* |c_i - c_{i-1}| <= diff_tol_a + diff_tol_r c_i   */
   QF_PLATEAU_LONG = 3,  /* c_{i-L} - c_i <= long_diff_r c_{i-L}, L = count  */
   QF_MAX_ITER = 4,      /* i == max_iters                                   */
-  QF_NUMERIC_FAIL = 5   /* Delta became non-finite                          */
+  QF_NUMERIC_FAIL = 5,  /* Delta became non-finite                          */
+  QF_BATCH_STOPPED = 6  /* batch policy only: another start converged       */
 } qf_verdict;
+
+/* Batch termination policy (NEXT-1; DESIGN.md reading
+ * R22), qf_params.batch_policy:
+ *   QF_BATCH_PER_START (0): every start runs to its own verdict (default; the
+ *     per-start verdicts do not depend on batching or sharding);
+ *   QF_BATCH_PAPER (1): all starts of the batch advance sweep by sweep
+ *     together; after each sweep the batch stops if any start converged,
+ *     or if every running start has hit a plateau at least once (a start
+ *     whose plateau test fires keeps iterating and may still converge), or
+ *     at max_iters.  Verdicts then: CONVERGED for converged starts, the
+ *     first plateau kind for plateaued ones, BATCH_STOPPED (stop on another
+ *     start's convergence) or MAX_ITER for the rest; NUMERIC_FAIL starts
+ *     stop on their own and do not hold the batch.  Streaming engine only.
+ * With several processes (one shard of the batch each), the per-sweep
+ * counts are summed over the batch by a caller-supplied reduction. */
+typedef enum { QF_BATCH_PER_START = 0, QF_BATCH_PAPER = 1 } qf_batch_policy;
+
+/* Sums counts[0..n) in place over every process of the batch (e.g. an
+ * all-reduce over the torch.distributed group); returns 0 on success.
+ * Called once per sweep from the thread that called qf_instantiate*; the
+ * counts are: [0] starts that converged this sweep, [1] running starts that
+ * have not yet hit a plateau, [2] running starts. */
+typedef int (*qf_batch_reduce_fn)(void *user, int64_t *counts, int32_t n);
 
 /* Which device engine runs the sweep. */
 typedef enum {
@@ -94,6 +118,9 @@ typedef struct {
   const int32_t *record_starts; /* record_count local start indices        */
   int32_t profile;        /* 1: time every k_sandwich / k_env_polar launch  */
                           /*    with CUDA events on the call's stream       */
+  int32_t batch_policy;   /* qf_batch_policy (default QF_BATCH_PER_START)   */
+  qf_batch_reduce_fn batch_reduce; /* NULL: this call is the whole batch   */
+  void *batch_user;       /* passed to batch_reduce                         */
 } qf_params;
 
 /* Per-start summary, 16 bytes (allgathered across ranks). */

@@ -23,7 +23,7 @@ _SRC = os.path.join(_HERE, "qf_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 VARIABLE, CONSTANT = 0, 1
-RUNNING, CONVERGED, PLATEAU_SHORT, PLATEAU_LONG, MAX_ITER, NUMERIC_FAIL = range(6)
+RUNNING, CONVERGED, PLATEAU_SHORT, PLATEAU_LONG, MAX_ITER, NUMERIC_FAIL, BATCH_STOPPED = range(7)
 
 
 def build(force: bool = False) -> str:
@@ -98,6 +98,10 @@ def _declare(L):
         ctypes.POINTER(_Circuit), _D, ctypes.c_int, _D, ctypes.POINTER(Params),
         ctypes.c_int, ctypes.c_int, ctypes.c_int, _D, _I, _I, _D, _D, _D]
     L.oracle_instantiate.restype = ctypes.c_int
+    L.oracle_instantiate_batch.argtypes = [
+        ctypes.POINTER(_Circuit), _D, ctypes.c_int, _D, ctypes.POINTER(Params),
+        ctypes.c_int, _D, _I, _I, _D]
+    L.oracle_instantiate_batch.restype = ctypes.c_int
 
 
 def _dp(a: np.ndarray):
@@ -265,3 +269,24 @@ def instantiate(circ: Circuit, target: np.ndarray, initial: np.ndarray,
         _dp(gh) if gh is not None else None)
     return Result(delta, iters, verdict, gates, ch[:, :R],
                   gh[:, :Rg] if gh is not None else None, th)
+
+
+def instantiate_batch(circ: Circuit, target: np.ndarray, initial: np.ndarray,
+                      params: Params | None = None, nthreads: int = 0) -> Result:
+    """The paper's GPU multistart termination (reading R22): all
+    starts advance sweep by sweep; stop on the first convergence, or once
+    every running start has hit a plateau, or at max_iters."""
+    params = params or default_params()
+    c, keep = circ._c()
+    initial = np.ascontiguousarray(initial, dtype=np.float64)
+    S = initial.shape[0]
+    var = circ.var_doubles
+    assert initial.shape == (S, var), (initial.shape, var)
+    delta = np.zeros(S)
+    iters = np.zeros(S, dtype=np.int32)
+    verdict = np.zeros(S, dtype=np.int32)
+    gates = np.zeros((S, var))
+    th = lib().oracle_instantiate_batch(
+        ctypes.byref(c), _dp(_cplx(target)), S, _dp(initial), ctypes.byref(params),
+        int(nthreads), _dp(delta), _ip(iters), _ip(verdict), _dp(gates))
+    return Result(delta, iters, verdict, gates, np.zeros((S, 0)), None, th)

@@ -500,3 +500,133 @@ int oracle_instantiate(const oracle_circuit *c, const double *target, int S,
   free(th);
   return nthreads;
 }
+
+/* ------------------------------------------------------------------ */
+/* Batch termination policy, see qf_oracle.h                */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const oracle_circuit *c;
+  const double *target;
+  const oracle_params *prm;
+  int S, var, it, nthreads;
+  double *ct;   /* S x 2 N^2 */
+  double *cost; /* S x (max_iters + 1) */
+  double *gates;
+  int *state;   /* ORACLE_RUNNING or the start's own final verdict */
+  int *event;   /* oracle_terminate after this sweep */
+  int reset;    /* rebuild the running starts' tensors (this pass) */
+} batch_t;
+
+typedef struct {
+  batch_t *B;
+  int t;
+} batch_arg;
+
+static void *batch_worker(void *arg) {
+  batch_arg *a = (batch_arg *)arg;
+  batch_t *B = a->B;
+  const int N = 1 << B->c->n;
+  const size_t NN2 = 2 * (size_t)N * N, ld = (size_t)B->prm->max_iters + 1;
+  for (int s = a->t; s < B->S; s += B->nthreads) {
+    if (B->state[s] != ORACLE_RUNNING) continue;
+    double *ct = B->ct + (size_t)s * NN2, *g = B->gates + (size_t)s * B->var;
+    double *cost = B->cost + (size_t)s * ld;
+    if (B->reset) {
+      oracle_init_ct(B->c, B->target, g, ct);
+      continue;
+    }
+    oracle_sweep(B->c, ct, g, B->prm->beta, 0);
+    cost[B->it] = delta_of(B->c->n, ct);
+    B->event[s] = oracle_terminate(B->prm, B->it, cost);
+  }
+  return 0;
+}
+
+static void batch_pass(batch_t *B) {
+  pthread_t th[256];
+  batch_arg args[256];
+  for (int t = 0; t < B->nthreads; t++) {
+    args[t].B = B;
+    args[t].t = t;
+    pthread_create(&th[t], 0, batch_worker, &args[t]);
+  }
+  for (int t = 0; t < B->nthreads; t++) pthread_join(th[t], 0);
+}
+
+int oracle_instantiate_batch(const oracle_circuit *c, const double *target, int S,
+                             const double *initial, const oracle_params *prm,
+                             int nthreads, double *delta, int *iters, int *verdict,
+                             double *gates_out) {
+  if (nthreads <= 0) nthreads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+  if (nthreads > S) nthreads = S;
+  if (nthreads > 256) nthreads = 256;
+  if (nthreads < 1) nthreads = 1;
+  const int N = 1 << c->n, var = oracle_var_doubles(c);
+  const size_t NN2 = 2 * (size_t)N * N, ld = (size_t)prm->max_iters + 1;
+  batch_t B;
+  B.c = c;
+  B.target = target;
+  B.prm = prm;
+  B.S = S;
+  B.var = var;
+  B.nthreads = nthreads;
+  B.ct = (double *)malloc(sizeof(double) * NN2 * S);
+  B.cost = (double *)malloc(sizeof(double) * ld * S);
+  B.gates = gates_out;
+  B.state = (int *)calloc(S, sizeof(int));
+  B.event = (int *)calloc(S, sizeof(int));
+  int *plat = (int *)calloc(S, sizeof(int));
+  memcpy(gates_out, initial, sizeof(double) * (size_t)S * var);
+  for (int s = 0; s < S; s++) {
+    oracle_init_ct(c, target, gates_out + (size_t)s * var, B.ct + (size_t)s * NN2);
+    B.cost[(size_t)s * ld] = delta_of(c->n, B.ct + (size_t)s * NN2);
+    iters[s] = 0;
+    delta[s] = B.cost[(size_t)s * ld];
+  }
+  if (prm->max_iters == 0) {
+    for (int s = 0; s < S; s++) verdict[s] = ORACLE_MAX_ITER;
+  } else {
+    for (int it = 1;; it++) {
+      B.it = it;
+      B.reset = 0;
+      batch_pass(&B);
+      int any_conv = 0, not_plat = 0;
+      for (int s = 0; s < S; s++) {
+        if (B.state[s] != ORACLE_RUNNING) continue;
+        const int e = B.event[s];
+        iters[s] = it;
+        delta[s] = B.cost[(size_t)s * ld + it];
+        if (e == ORACLE_NUMERIC_FAIL) {
+          B.state[s] = verdict[s] = ORACLE_NUMERIC_FAIL;
+          continue;
+        }
+        if (e == ORACLE_CONVERGED) {
+          any_conv = 1;
+          continue;
+        }
+        if ((e == ORACLE_PLATEAU_SHORT || e == ORACLE_PLATEAU_LONG) && plat[s] == 0) plat[s] = e;
+        if (plat[s] == 0) not_plat++;
+      }
+      if (any_conv || not_plat == 0 || it >= prm->max_iters) {
+        for (int s = 0; s < S; s++) {
+          if (B.state[s] != ORACLE_RUNNING) continue;
+          verdict[s] = B.event[s] == ORACLE_CONVERGED ? ORACLE_CONVERGED
+                       : plat[s]                        ? plat[s]
+                       : any_conv                       ? ORACLE_BATCH_STOPPED
+                                                        : ORACLE_MAX_ITER;
+        }
+        break;
+      }
+      if (prm->reset_iters > 0 && it % prm->reset_iters == 0) {
+        B.reset = 1;
+        batch_pass(&B);
+      }
+    }
+  }
+  free(plat);
+  free(B.event);
+  free(B.state);
+  free(B.cost);
+  free(B.ct);
+  return nthreads;
+}

@@ -36,7 +36,8 @@ enum {
   ORACLE_PLATEAU_SHORT = 2,
   ORACLE_PLATEAU_LONG = 3,
   ORACLE_MAX_ITER = 4,
-  ORACLE_NUMERIC_FAIL = 5
+  ORACLE_NUMERIC_FAIL = 5,
+  ORACLE_BATCH_STOPPED = 6
 };
 
 /* Hyperparameters of Sec. 3.1.2. */
@@ -107,6 +108,20 @@ int oracle_instantiate(const oracle_circuit *c, const double *target, int S,
                        double *delta, int *iters, int *verdict,
                        double *gates_out, double *cost_hist,
                        double *gates_hist);
+
+/* The paper's GPU multistart termination (DESIGN.md
+ * reading R22): all S starts advance one sweep at a time.  After sweep `it`
+ * each running start is tested with oracle_terminate: NUMERIC_FAIL stops
+ * that start alone; CONVERGED marks it; a plateau verdict is remembered
+ * (first kind) but the start keeps iterating.  The batch then stops if any
+ * start converged, or if every running start has hit a plateau, or at
+ * max_iters; the running starts get CONVERGED / their first plateau kind /
+ * BATCH_STOPPED (another start converged) / MAX_ITER.  Resets as in
+ * oracle_instantiate.  Same outputs (no records); returns the thread count. */
+int oracle_instantiate_batch(const oracle_circuit *c, const double *target, int S,
+                             const double *initial, const oracle_params *prm,
+                             int nthreads, double *delta, int *iters, int *verdict,
+                             double *gates_out);
 
 #ifdef __cplusplus
 }

@@ -21,12 +21,14 @@ from . import _build
 
 QF_OK, QF_E_ARG, QF_E_DIM, QF_E_LOCATION, QF_E_NOT_UNITARY, QF_E_OOM, QF_E_CUDA, QF_E_NCCL = range(8)
 QF_GATE_VARIABLE, QF_GATE_CONSTANT = 0, 1
-QF_RUNNING, QF_CONVERGED, QF_PLATEAU_SHORT, QF_PLATEAU_LONG, QF_MAX_ITER, QF_NUMERIC_FAIL = range(6)
+(QF_RUNNING, QF_CONVERGED, QF_PLATEAU_SHORT, QF_PLATEAU_LONG, QF_MAX_ITER, QF_NUMERIC_FAIL,
+ QF_BATCH_STOPPED) = range(7)
 QF_ENGINE_AUTO, QF_ENGINE_STREAM, QF_ENGINE_RESIDENT = range(3)
+QF_BATCH_PER_START, QF_BATCH_PAPER = range(2)
 
 ENGINE_NAMES = {0: "auto", 1: "stream", 2: "resident"}
 VERDICT_NAMES = {0: "RUNNING", 1: "CONVERGED", 2: "PLATEAU_SHORT", 3: "PLATEAU_LONG",
-                 4: "MAX_ITER", 5: "NUMERIC_FAIL"}
+                 4: "MAX_ITER", 5: "NUMERIC_FAIL", 6: "BATCH_STOPPED"}
 
 EXPORTS = [
     "qf_params_default", "qf_circuit_create", "qf_circuit_destroy", "qf_circuit_var_doubles",
@@ -41,6 +43,11 @@ class QfError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"qf status {status}: {msg}")
         self.status = status
+
+
+# qf_batch_reduce_fn: sums int64 counts[0..n) in place over the batch's processes
+BATCH_REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.c_int32)
 
 
 class qf_params(ctypes.Structure):
@@ -60,6 +67,9 @@ class qf_params(ctypes.Structure):
         ("record_count", ctypes.c_int32),
         ("record_starts", ctypes.POINTER(ctypes.c_int32)),
         ("profile", ctypes.c_int32),
+        ("batch_policy", ctypes.c_int32),
+        ("batch_reduce", BATCH_REDUCE_FN),
+        ("batch_user", ctypes.c_void_p),
     ]
 
 

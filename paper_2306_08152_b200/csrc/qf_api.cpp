@@ -146,6 +146,10 @@ qf_status check_params(const qf_circuit_s *c, const qf_params *p) {
     return fail(QF_E_ARG, "the resident engine holds the tensor in shared memory: n <= 6");
   if (p->engine == QF_ENGINE_RESIDENT && c->p > 240)
     return fail(QF_E_ARG, "the resident engine takes at most 240 gates");
+  if (p->batch_policy != QF_BATCH_PER_START && p->batch_policy != QF_BATCH_PAPER)
+    return fail(QF_E_ARG, "batch_policy must be QF_BATCH_PER_START or QF_BATCH_PAPER");
+  if (p->batch_policy == QF_BATCH_PAPER && p->engine == QF_ENGINE_RESIDENT)
+    return fail(QF_E_ARG, "the batch policy runs sweep-synchronously on the streaming engine");
   if (p->record_sweeps < 0 || p->record_count < 0)
     return fail(QF_E_ARG, "record_sweeps and record_count must be >= 0");
   if (p->record_count > 0 && p->record_sweeps > 0) {
@@ -187,6 +191,9 @@ void qf_params_default(qf_params *p) {
   p->record_sweeps = 0;
   p->record_count = 0;
   p->record_starts = nullptr;
+  p->batch_policy = QF_BATCH_PER_START;
+  p->batch_reduce = nullptr;
+  p->batch_user = nullptr;
 }
 
 qf_status qf_circuit_create(int num_qubits, int num_gates, const int *arity,

@@ -217,7 +217,7 @@ std::pair<int, int> row_tiles(int n, int m) {
 struct Layout {
   size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
       rec_slot, rec_starts, rec_cost, rec_gates, summary, best, part, tpart, vstore, vslots,
-      gdesc, total;
+      gdesc, plat, total;
   long long vstride;  // complex per start in vstore (sum over VARIABLE gates of 2 d^2)
   int nvslots;
   int ring;
@@ -268,6 +268,7 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
   L.vstore = take(std::max<size_t>(1, S * (size_t)L.vstride) * 16);
   L.vslots = take((size_t)std::max(1, L.nvslots) * 8);
   L.gdesc = take((size_t)std::max(1, c.p) * sizeof(GateDesc));
+  L.plat = take(S * 4);
   L.total = o;
   return L;
 }
@@ -357,6 +358,8 @@ struct Engine {
   int *active() const { return reinterpret_cast<int *>(ws + L.active); }
   int *n_active() const { return reinterpret_cast<int *>(ws + L.counters); }
   int *bad() const { return reinterpret_cast<int *>(ws + L.counters) + 1; }
+  unsigned *batch_counts() const { return reinterpret_cast<unsigned *>(ws + L.counters) + 4; }
+  int *plat() const { return reinterpret_cast<int *>(ws + L.plat); }
 
   Engine(const qf_circuit_s &c_, const qf_params &p_, cudaStream_t st_, void *ws_)
       : c(c_), p(p_), st(st_), ws(static_cast<char *>(ws_)), L(make_layout(c_, p_)) {
@@ -708,6 +711,9 @@ struct Engine {
       A.tpart_tiles = tpart_tiles;
     }
     tpart_tiles = 0;
+    A.batch = p.batch_policy == QF_BATCH_PAPER ? 1 : 0;
+    A.plat = plat();
+    A.counts = batch_counts();
     const int g = std::max(1, std::min((S + kTraceWarps - 1) / kTraceWarps, nsm * 8));
     k_trace_mask<<<g, 32 * kTraceWarps, 0, st>>>(A);
     launches++;
@@ -806,7 +812,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   QF_CHECK(cudaGetLastError());
   // pinned host words: [0] input flags, [1 + j] = n_active after sweep j
   int *h_flags = nullptr;
-  QF_CHECK(cudaHostAlloc(&h_flags, ((size_t)p.max_iters + 3) * sizeof(int), cudaHostAllocDefault));
+  QF_CHECK(cudaHostAlloc(&h_flags, ((size_t)p.max_iters + 8) * sizeof(int), cudaHostAllocDefault));
   struct Pinned {
     int *p;
     ~Pinned() { cudaFreeHost(p); }
@@ -825,8 +831,9 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     return QF_E_NOT_UNITARY;
   }
 
+  const bool batch = p.batch_policy == QF_BATCH_PAPER;
   const bool resident = p.engine == QF_ENGINE_RESIDENT ||
-                        (p.engine == QF_ENGINE_AUTO && c.n <= kResidentMaxQubits &&
+                        (p.engine == QF_ENGINE_AUTO && !batch && c.n <= kResidentMaxQubits &&
                          c.p <= kResMaxGates);
   int last = 0;  // last sweep enqueued (streaming engine)
   cudaEvent_t ev[2];
@@ -916,6 +923,39 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   // ---- a3..a7: sweeps until every start has a verdict
   if (p.max_iters == 0) {
     QF_CHECK(E.trace(0));
+  } else if (batch) {
+    // ---- NEXT-1: sweep-synchronous batch; the host decides after every sweep
+    QF_CHECK(cudaMemsetAsync(E.plat(), 0, (size_t)S * 4, st));
+    unsigned *h_cnt = reinterpret_cast<unsigned *>(h_flags + p.max_iters + 4);  // 3 words
+    for (int it = 1; it <= p.max_iters; it++) {
+      E.ctx = it - 1;
+      for (int k = c.p - 1; k >= 0; k--) QF_CHECK(E.step(k, 0));
+      for (int k = 0; k < c.p; k++) QF_CHECK(E.step(k, 1));
+      QF_CHECK(cudaMemsetAsync(E.batch_counts(), 0, 3 * sizeof(unsigned), st));
+      QF_CHECK(E.trace(it));
+      E.ctx = it;
+      QF_CHECK(cudaMemcpyAsync(h_cnt, E.batch_counts(), 3 * sizeof(unsigned),
+                               cudaMemcpyDeviceToHost, st));
+      QF_CHECK(cudaMemcpyAsync(&h_nact[it], E.n_active(), sizeof(int), cudaMemcpyDeviceToHost, st));
+      d2h += 16;
+      QF_CHECK(cudaStreamSynchronize(st));
+      int64_t cnt[3] = {h_cnt[0], h_cnt[1], h_cnt[2]};
+      if (p.batch_reduce && p.batch_reduce(p.batch_user, cnt, 3) != 0) {
+        set_error("batch_reduce callback failed");
+        return QF_E_NCCL;
+      }
+      last = it;
+      const bool any_conv = cnt[0] > 0;
+      if (any_conv || cnt[1] == 0 || it == p.max_iters) {
+        k_batch_finalize<<<std::max(1, std::min((S + 255) / 256, E.nsm * 4)), 256, 0, st>>>(
+            reinterpret_cast<int *>(W + E.L.verdict), E.plat(), S, any_conv ? 1 : 0,
+            E.n_active());
+        E.launches++;
+        QF_CHECK(cudaGetLastError());
+        break;
+      }
+      if (p.reset_iters > 0 && it % p.reset_iters == 0) QF_CHECK(E.init_ct());
+    }
   } else {
     for (int it = 1; it <= p.max_iters; it++) {
       E.ctx = it - 1;  // this sweep runs on the starts active after sweep it-1

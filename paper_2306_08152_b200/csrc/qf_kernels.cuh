@@ -778,6 +778,12 @@ struct TraceArgs {
   const double2 *tpart;  // fused trace partials (nullptr: diagonal gather)
   long long tpart_stride;
   int tpart_tiles;
+  // batch policy (qf.h QF_BATCH_PAPER): plateaus do not stop a start; plat[s]
+  // keeps the first plateau kind; counts[0..3) += converged / running and
+  // not yet plateaued / running (see qf_batch_reduce_fn)
+  int batch;
+  int *plat;
+  unsigned *counts;
 };
 
 constexpr int kTraceWarps = 8;
@@ -831,6 +837,21 @@ __global__ void __launch_bounds__(32 * kTraceWarps) k_trace_mask(const TraceArgs
           }
           if (v == 0 && it >= A.max_iters) v = 4;
         }
+        if (A.batch) {
+          // the batch decides after the sweep (k_batch_finalize); only a
+          // converged or failed start leaves the active list here
+          if (v == 2 || v == 3) {
+            if (A.plat[s] == 0) A.plat[s] = v;
+            v = 0;
+          } else if (v == 4) {
+            v = 0;
+          }
+          if (v != 5) {
+            atomicAdd(&A.counts[2], 1u);
+            if (v == 1) atomicAdd(&A.counts[0], 1u);
+            else if (A.plat[s] == 0) atomicAdd(&A.counts[1], 1u);
+          }
+        }
       }
       A.delta[s] = c;
       A.iters[s] = it;
@@ -846,6 +867,16 @@ __global__ void __launch_bounds__(32 * kTraceWarps) k_trace_mask(const TraceArgs
       }
     }
   }
+}
+
+// Batch policy: the batch stops after this sweep (the host summed the counts
+// over every shard): each start still running takes its first plateau kind,
+// else BATCH_STOPPED when some start of the batch converged, else MAX_ITER.
+__global__ void k_batch_finalize(int *verdict, const int *plat, int S, int any_conv,
+                                 int *n_active) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
+    if (verdict[s] == 0) verdict[s] = plat[s] != 0 ? plat[s] : (any_conv ? 6 : 4);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_active = 0;
 }
 
 // Stable in-place compaction of the active list: keep starts still RUNNING.

@@ -1,7 +1,9 @@
 """Multi-start sharding across GPUs: plumbing only.
 
-Starts are independent, so ranks exchange nothing during the sweeps.  At the
-end of a run: NCCL allgather of the per-start 16-byte summaries, the argmin
+Starts are independent, so under the per-start policy ranks exchange nothing
+during the sweeps.  Under the paper's batch policy (NEXT-1) the
+ranks' shards form one batch: after every sweep the library calls a reducer
+that sums three counts over the group (`batch_reducer`).  At the end of a run: NCCL allgather of the per-start 16-byte summaries, the argmin
 kernel (qf_select_best_device) on the gathered table, and a broadcast of the
 winner's gates from the rank that owns it.  One process per GPU, launched by
 torchrun; torch.distributed provides the process group.
@@ -13,7 +15,7 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
-from . import qf_select_best_device
+from . import BATCH_REDUCE_FN, qf_select_best_device
 
 
 @dataclass
@@ -60,3 +62,35 @@ def exchange_best(shard: Shard, summ: torch.Tensor, gates_out: torch.Tensor, str
         buf = torch.empty(gates_out.shape[1], dtype=gates_out.dtype, device=gates_out.device)
     dist.broadcast(buf, src=owner)
     return best, buf
+
+
+def reduce_counts(counts, group=None, device=None):
+    """Sum a small int64 vector over the process group (in place on a host
+    tensor); NCCL groups reduce a device copy."""
+    t = torch.as_tensor(counts, dtype=torch.int64)
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        d = t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(d, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(d.cpu())
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def batch_reducer(group=None, device=None):
+    """A qf_batch_reduce_fn (qf.h) for qf_params.batch_reduce that sums the
+    per-sweep batch counts over `group`.  Keep the returned object alive for
+    the duration of the call."""
+
+    def _fn(user, counts, n):
+        try:
+            vals = [int(counts[i]) for i in range(n)]
+            out = reduce_counts(vals, group, device)
+            for i in range(n):
+                counts[i] = int(out[i])
+            return 0
+        except Exception:  # reported to the caller as QF_E_NCCL
+            return 1
+
+    return BATCH_REDUCE_FN(_fn)

@@ -70,7 +70,10 @@ def test_param_validation_precedes_device():
     V = w.target_unitary()
     g = w.initial()
     for bad, status in (({"beta": 1.5}, qf.QF_E_ARG), ({"dist_tol": 0.0}, qf.QF_E_ARG),
-                        ({"max_iters": -1}, qf.QF_E_ARG), ({"reset_iters": 0}, qf.QF_E_ARG)):
+                        ({"max_iters": -1}, qf.QF_E_ARG), ({"reset_iters": 0}, qf.QF_E_ARG),
+                        ({"batch_policy": 2}, qf.QF_E_ARG),
+                        ({"batch_policy": qf.QF_BATCH_PAPER, "engine": qf.QF_ENGINE_RESIDENT},
+                         qf.QF_E_ARG)):
         with pytest.raises(qf.QfError) as e:
             qf.qf_instantiate(c, V, g, **bad)
         assert e.value.status == status

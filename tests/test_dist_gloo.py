@@ -74,3 +74,41 @@ def test_shard_ranges():
             assert max(sizes) - min(sizes) <= 1
     s = Shard(3, 8, 4096)
     assert s.start_begin == 3 * 4096 and s.owner(3 * 4096 + 17) == (3, 17)
+
+
+def _batch_worker(rank, world, port, q):
+    """The batch-policy reducer (qf_params.batch_reduce) called the way the
+    library calls it: through the C function pointer, on int64 counts."""
+    import ctypes
+
+    from paper_2306_08152_b200.dist import batch_reducer
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fn = batch_reducer()
+        # rank 0: one start converged, 3 running, 2 not plateaued; rank 1: none
+        # converged, 5 running, 0 not plateaued
+        local = [1, 2, 3] if rank == 0 else [0, 0, 5]
+        arr = (ctypes.c_int64 * 3)(*local)
+        rc = fn(None, ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64)), 3)
+        q.put((rank, rc, list(arr)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batch_reducer_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for rank, rc, counts in out:
+        assert rc == 0
+        assert counts == [1, 2, 8]  # summed over the batch on every rank
