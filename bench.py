@@ -121,6 +121,9 @@ def config_dict(w, world):
                "vs 126 MB L2, no flush" if w.starts * 16 * 4 ** w.n > 126e6 else
                "working set fits in L2 (reported as such)"),
         "parallelism": f"starts sharded over {world} GPU(s), weak scaling",
+        "termination": ("paper batch policy (P:667-676): all starts of the job stop on the first "
+                        "success, plateau-stop once every start has plateaued"
+                        if getattr(w, "batch", "per-start") == "paper" else "per-start verdicts"),
     }
 
 
@@ -134,7 +137,10 @@ def oracle_sample(w, starts, threads):
     init = w.initial(0, starts)
     P = oracle.default_params(max_iters=w.max_iters)
     t0 = time.perf_counter()
-    r = oracle.instantiate(c, V, init, P, nthreads=threads)
+    if getattr(w, "batch", "per-start") == "paper":
+        r = oracle.instantiate_batch(c, V, init, P, nthreads=threads)
+    else:
+        r = oracle.instantiate(c, V, init, P, nthreads=threads)
     dt = time.perf_counter() - t0
     return dt, r
 
@@ -234,10 +240,13 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "stream", "resident"],
                     help="device engine (auto: resident for n <= 6)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--batch", default="per-start", choices=["per-start", "paper"],
+                    help="termination: per-start verdicts, or the paper's batch policy (NEXT-1)")
     args = ap.parse_args()
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     w = qfgen.workload(args.config)
+    w.batch = args.batch
     if args.max_iters is not None:
         w.max_iters = args.max_iters
     if args.impl == "reference":
@@ -268,11 +277,17 @@ def main():
     summ = torch.empty(S * 16, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     shard = qfdist.Shard(rank, world, S)
+    bparams = {}
+    if args.batch == "paper":
+        bparams["batch_policy"] = qf.QF_BATCH_PAPER
+        if world > 1:  # the job's starts form one batch: per-sweep count all-reduce
+            reducer = qfdist.batch_reducer(device=dev)
+            bparams["batch_reduce"] = reducer
 
     def step(profile):
         r = qf.qf_instantiate_device(c, d_V, d_init, ws, stream, d_gates_out=gates_out,
                                      d_summary_out=summ, max_iters=w.max_iters, profile=profile,
-                                     engine=engine)
+                                     engine=engine, **bparams)
         best = qfdist.exchange_best(shard, summ, gates_out, stream) if world > 1 else None
         return r, best
 
@@ -321,12 +336,12 @@ def main():
         h_init = torch.from_numpy(init).pin_memory()
         for _ in range(1):
             qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters,
-                                  engine=engine)
+                                  engine=engine, **bparams)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         rr = [qf.qf_instantiate_ptr(c, h_V.data_ptr(), h_init.data_ptr(), S, max_iters=w.max_iters,
-                                    engine=engine)
+                                    engine=engine, **bparams)
               for _ in range(args.steps)]
         t_e2e = time.perf_counter() - t0
         tv = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
