@@ -176,6 +176,25 @@ qf_status qf_instantiate(qf_circuit_t c, const double *target,
                          const double *initial, const qf_params *p,
                          qf_result_t *out);
 
+/* NEXT-2: heterogeneous batched instantiation --
+ * num_problems independent problems, each with its own template
+ * circuits[q], target targets[q] (N_q x N_q complex, host) and
+ * num_starts[q] starts initials[q] (num_starts[q] x var_doubles(q), host),
+ * in ONE persistent resident-engine launch: CTAs take (problem, start)
+ * work items from one counter, so small blocks share the GPU without
+ * process-level packing (the paper's MPS).  Hyperparameters p are shared
+ * (p->num_starts is ignored).  Every circuit must satisfy the resident
+ * engine (n <= 6); no per-sweep records, per-start batch policy only.  Each
+ * start's arithmetic is that of a single-problem resident call, so results
+ * are bitwise those of running problem q alone.  out[q] receives problem
+ * q's result (every start's gates held on the host), or NULL on error.
+ * Blocking; runs on the current CUDA device.  Errors: QF_E_ARG, QF_E_DIM,
+ * QF_E_NOT_UNITARY, QF_E_OOM, QF_E_CUDA. */
+qf_status qf_instantiate_many(int32_t num_problems, const qf_circuit_t *circuits,
+                              const double *const *targets, const double *const *initials,
+                              const int32_t *num_starts, const qf_params *p,
+                              qf_result_t *out);
+
 /* Device workspace, in bytes, that qf_instantiate_device needs. */
 size_t qf_workspace_size(qf_circuit_t c, const qf_params *p);
 

@@ -35,7 +35,7 @@ EXPORTS = [
     "qf_circuit_num_qubits", "qf_instantiate", "qf_workspace_size", "qf_instantiate_device",
     "qf_result_get", "qf_result_best", "qf_result_num_starts", "qf_result_trace",
     "qf_result_stats", "qf_result_destroy", "qf_select_best_device", "qf_select_best_host",
-    "qf_last_error", "qf_version",
+    "qf_last_error", "qf_version", "qf_instantiate_many",
 ]
 
 
@@ -144,6 +144,8 @@ def _declare(L):
     L.qf_result_destroy.restype = None
     L.qf_select_best_device.argtypes = [_VP, c.c_int64, _VP, _VP]
     L.qf_select_best_host.argtypes = [c.POINTER(qf_summary), c.c_int64, c.POINTER(c.c_int64)]
+    L.qf_instantiate_many.argtypes = [c.c_int32, c.POINTER(_VP), c.POINTER(_D), c.POINTER(_D),
+                                      _I, c.POINTER(qf_params), c.POINTER(_VP)]
     L.qf_last_error.restype = c.c_char_p
     L.qf_last_error.argtypes = []
     L.qf_version.restype = c.c_char_p
@@ -293,6 +295,35 @@ def qf_instantiate(circ: Circuit, target, initial, record_starts=None, record_sw
 
 
 instantiate = qf_instantiate
+
+
+def qf_instantiate_many(circuits, targets, initials, **params) -> list:
+    """NEXT-2: several problems (own template, target, starts) in one resident
+    launch (qf.h qf_instantiate_many).  Returns one Result per problem."""
+    P = len(circuits)
+    assert len(targets) == P and len(initials) == P
+    ts = [_cplx(t) for t in targets]
+    ins = [np.ascontiguousarray(x, dtype=np.float64) for x in initials]
+    for c, x in zip(circuits, ins):
+        assert x.ndim == 2 and x.shape[1] == c.var_doubles, (x.shape, c.var_doubles)
+    S = np.array([x.shape[0] for x in ins], dtype=np.int32)
+    p, _ = _make_params(1, **params)
+    hs = (_VP * P)(*[c.h for c in circuits])
+    tp = (_D * P)(*[t.ctypes.data_as(_D) for t in ts])
+    ip = (_D * P)(*[x.ctypes.data_as(_D) for x in ins])
+    out = (_VP * P)()
+    _check(lib().qf_instantiate_many(P, hs, tp, ip, S.ctypes.data_as(_I), ctypes.byref(p), out))
+    res = []
+    try:
+        for q in range(P):
+            res.append(_collect(out[q], circuits[q].var_doubles, True))
+    finally:
+        for q in range(P):
+            lib().qf_result_destroy(out[q])
+    return res
+
+
+instantiate_many = qf_instantiate_many
 
 
 def qf_workspace_size(circ: Circuit, S, **params) -> int:

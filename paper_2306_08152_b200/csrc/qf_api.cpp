@@ -408,6 +408,64 @@ qf_status qf_result_stats(qf_result_t r, qf_stats *stats) {
   return QF_OK;
 }
 
+qf_status qf_instantiate_many(int32_t num_problems, const qf_circuit_t *circuits,
+                              const double *const *targets, const double *const *initials,
+                              const int32_t *num_starts, const qf_params *p,
+                              qf_result_t *out) {
+  qf::g_err.clear();
+  if (!out) return fail(QF_E_ARG, "out is NULL");
+  if (num_problems < 1) return fail(QF_E_ARG, "num_problems must be >= 1");
+  for (int q = 0; q < num_problems; q++) out[q] = nullptr;
+  if (!circuits || !targets || !initials || !num_starts || !p)
+    return fail(QF_E_ARG, "circuits, targets, initials, num_starts and p must not be NULL");
+  if (p->record_sweeps > 0 && p->record_count > 0)
+    return fail(QF_E_ARG, "qf_instantiate_many keeps no per-sweep records");
+  if (p->batch_policy != QF_BATCH_PER_START)
+    return fail(QF_E_ARG, "qf_instantiate_many runs the per-start policy only");
+  if (p->engine == QF_ENGINE_STREAM)
+    return fail(QF_E_ARG, "qf_instantiate_many runs on the resident engine");
+  for (int q = 0; q < num_problems; q++) {
+    qf_circuit_s *c = circuits[q];
+    if (!c) return fail(QF_E_ARG, "circuit " + std::to_string(q) + " is NULL");
+    if (c->n > 6) return fail(QF_E_ARG, "problem " + std::to_string(q) + ": n > 6 (resident engine)");
+    if (num_starts[q] < 0) return fail(QF_E_ARG, "num_starts must be >= 0");
+    qf_params pq = *p;
+    pq.num_starts = std::max(1, num_starts[q]);
+    pq.engine = QF_ENGINE_AUTO;
+    qf_status s = check_params(c, &pq);
+    if (s != QF_OK) return s;
+    if (!targets[q]) return fail(QF_E_ARG, "target " + std::to_string(q) + " is NULL");
+    if (!initials[q] && c->var_doubles > 0 && num_starts[q] > 0)
+      return fail(QF_E_ARG, "initial " + std::to_string(q) + " is NULL");
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev < 1) return fail(QF_E_CUDA, "no CUDA device available");
+  qf::retain_device_pool();
+  cudaStream_t st = nullptr;
+  if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
+    return qf::cuda_fail(e, "cudaStreamCreate");
+  std::vector<qf_result_s *> res(num_problems, nullptr);
+  qf_status s = QF_OK;
+  for (int q = 0; q < num_problems && s == QF_OK; q++) {
+    res[q] = new (std::nothrow) qf_result_s();
+    if (!res[q]) s = fail(QF_E_OOM, "host allocation failed");
+  }
+  if (s == QF_OK) {
+    std::vector<const qf_circuit_s *> cs(circuits, circuits + num_problems);
+    s = qf::engine_run_many(num_problems, cs.data(), targets, initials, num_starts, *p, st,
+                            res.data());
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (s != QF_OK) {
+    for (auto *r : res) delete r;
+    return s;
+  }
+  for (int q = 0; q < num_problems; q++) out[q] = res[q];
+  return QF_OK;
+}
+
 void qf_result_destroy(qf_result_t r) { delete r; }
 
 qf_status qf_select_best_device(const qf_summary *d_summaries, int64_t count, void *stream,

@@ -727,6 +727,24 @@ struct Engine {
 
 }  // namespace
 
+// gate descriptors of the resident engine (voff: warm-start slots or null)
+std::vector<GateDesc> make_gdesc(const qf_circuit_s &c, const std::vector<int> *voff) {
+  std::vector<GateDesc> gd(c.p);
+  for (int k = 0; k < c.p; k++) {
+    const Bits b = make_bits(c, k);
+    GateDesc &g = gd[k];
+    g.m = b.m;
+    g.d = b.d;
+    g.kind = c.kind[k] == QF_GATE_VARIABLE ? 0 : 1;
+    g.goff = g.kind == 0 ? c.var_off[k] / 2 : c.const_off[k] / 2;
+    g.mask = b.abits[b.d - 1];
+    g.voff = voff && g.kind == 0 ? (*voff)[k] : 0;
+    for (int a = 0; a < 8; a++) g.abits[a] = a < b.d ? b.abits[a] : 0;
+    for (int q = 0; q < kMaxQubits; q++) g.rest_pos[q] = q < c.n - b.m ? b.rest_pos[q] : 0;
+  }
+  return gd;
+}
+
 size_t engine_workspace_size(const qf_circuit_s &c, const qf_params &p) {
   return make_layout(c, p).total;
 }
@@ -848,19 +866,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   } events{ev};
   if (resident) {
     // ---- a2..a7 in one kernel: one CTA per start, tensor in shared memory
-    std::vector<GateDesc> gd(c.p);
-    for (int k = 0; k < c.p; k++) {
-      const Bits b = make_bits(c, k);
-      GateDesc &g = gd[k];
-      g.m = b.m;
-      g.d = b.d;
-      g.kind = c.kind[k] == QF_GATE_VARIABLE ? 0 : 1;
-      g.goff = g.kind == 0 ? c.var_off[k] / 2 : c.const_off[k] / 2;
-      g.mask = b.abits[b.d - 1];
-      g.voff = E.warm && g.kind == 0 ? E.voff[k] : 0;
-      for (int a = 0; a < 8; a++) g.abits[a] = a < b.d ? b.abits[a] : 0;
-      for (int q = 0; q < kMaxQubits; q++) g.rest_pos[q] = q < c.n - b.m ? b.rest_pos[q] : 0;
-    }
+    const std::vector<GateDesc> gd = make_gdesc(c, E.warm ? &E.voff : nullptr);
     QF_CHECK(cudaMemcpyAsync(W + E.L.gdesc, gd.data(), gd.size() * sizeof(GateDesc),
                              cudaMemcpyHostToDevice, st));
     h2d += (long long)(gd.size() * sizeof(GateDesc));
@@ -904,7 +910,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     const size_t smem = (size_t)N * N * 16 + 8 * 64 * 16;
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
-    auto kern = maxm == 1 ? k_resident<2> : maxm == 2 ? k_resident<4> : k_resident<8>;
+    auto kern = maxm == 1 ? k_resident<2, false> : maxm == 2 ? k_resident<4, false> : k_resident<8, false>;
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
@@ -1085,6 +1091,256 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     r.stats.d2h_bytes += d2h;
   } else {
     QF_CHECK(cudaStreamSynchronize(st));
+  }
+  return QF_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-2
+// Many problems (own template, target, starts) in one persistent resident
+// launch: k_resident<MAXD, true> takes (problem, start) work items from one
+// counter; each start reads its problem's tables from global memory.  Per
+// start the arithmetic is that of a single-problem launch.
+qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *const *targets,
+                          const double *const *initials, const int *S, const qf_params &p,
+                          cudaStream_t st, qf_result_s *const *outs) {
+  int dev = 0, nsm = 0;
+  QF_CHECK(cudaGetDevice(&dev));
+  QF_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int ring = std::max(kRingMin, p.long_diff_count + 1);
+  int maxn = 1, maxm = 1;
+  long long Stot = 0;
+  std::vector<long long> start0(np);
+  for (int q = 0; q < np; q++) {
+    maxn = std::max(maxn, cs[q]->n);
+    for (int k = 0; k < cs[q]->p; k++) maxm = std::max(maxm, cs[q]->arity[k]);
+    start0[q] = Stot;
+    Stot += S[q];
+  }
+  if (Stot > INT32_MAX) {
+    set_error("too many starts in one launch");
+    return QF_E_ARG;
+  }
+  // one stream-ordered allocation
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + std::max<size_t>(bytes, 1));
+    return at;
+  };
+  struct Off {
+    size_t tgt, vdag, cm, gd, gates, gtab;
+    std::vector<GateDesc> desc;
+    std::vector<int2> tab;
+  };
+  std::vector<Off> off(np);
+  for (int q = 0; q < np; q++) {
+    const qf_circuit_s &c = *cs[q];
+    const size_t N = (size_t)1 << c.n;
+    off[q].desc = make_gdesc(c, nullptr);
+    for (int k = 0; k < c.p; k++)
+      if (c.kind[k] == QF_GATE_VARIABLE) off[q].tab.push_back(make_int2(c.var_off[k], 1 << c.arity[k]));
+    off[q].tgt = take(N * N * 16);
+    off[q].vdag = take(N * N * 16);
+    off[q].cm = take(c.const_mats.size() * 8);
+    off[q].gd = take(off[q].desc.size() * sizeof(GateDesc));
+    off[q].gates = take((size_t)S[q] * c.var_doubles * 8);
+    off[q].gtab = take(off[q].tab.size() * sizeof(int2));
+  }
+  const size_t o_probs = take((size_t)np * sizeof(ResProb));
+  const size_t o_hist = take((size_t)Stot * ring * 8);
+  const size_t o_delta = take((size_t)Stot * 8);
+  const size_t o_iters = take((size_t)Stot * 4);
+  const size_t o_verdict = take((size_t)Stot * 4);
+  const size_t o_cnt = take(64);
+  char *W = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&W), o, st);
+  if (e != cudaSuccess) {
+    set_error(std::string("device allocation failed: ") + cudaGetErrorString(e));
+    return QF_E_OOM;
+  }
+  struct Free {
+    char *w;
+    cudaStream_t st;
+    ~Free() {
+      cudaFreeAsync(w, st);
+      cudaStreamSynchronize(st);
+    }
+  } guard{W, st};
+  long long h2d = 0, d2h = 0, launches = 0;
+  int *bad = reinterpret_cast<int *>(W + o_cnt), *counter = bad + 1;
+  QF_CHECK(cudaMemsetAsync(W + o_cnt, 0, 64, st));
+  std::vector<ResProb> probs(np);
+  for (int q = 0; q < np; q++) {
+    const qf_circuit_s &c = *cs[q];
+    const int N = 1 << c.n;
+    const size_t NN = (size_t)N * N;
+    QF_CHECK(cudaMemcpyAsync(W + off[q].tgt, targets[q], NN * 16, cudaMemcpyHostToDevice, st));
+    if (c.var_doubles > 0)
+      QF_CHECK(cudaMemcpyAsync(W + off[q].gates, initials[q], (size_t)S[q] * c.var_doubles * 8,
+                               cudaMemcpyHostToDevice, st));
+    if (!c.const_mats.empty())
+      QF_CHECK(cudaMemcpyAsync(W + off[q].cm, c.const_mats.data(), c.const_mats.size() * 8,
+                               cudaMemcpyHostToDevice, st));
+    if (!off[q].desc.empty())
+      QF_CHECK(cudaMemcpyAsync(W + off[q].gd, off[q].desc.data(),
+                               off[q].desc.size() * sizeof(GateDesc), cudaMemcpyHostToDevice, st));
+    if (!off[q].tab.empty())
+      QF_CHECK(cudaMemcpyAsync(W + off[q].gtab, off[q].tab.data(), off[q].tab.size() * sizeof(int2),
+                               cudaMemcpyHostToDevice, st));
+    h2d += (long long)(NN * 16 + (size_t)S[q] * c.var_doubles * 8 + c.const_mats.size() * 8 +
+                       off[q].desc.size() * sizeof(GateDesc) + off[q].tab.size() * sizeof(int2));
+    const double2 *tg = reinterpret_cast<const double2 *>(W + off[q].tgt);
+    const int g1 = std::max(1, std::min((int)((NN + 255) / 256), nsm * 8));
+    k_vdag<<<g1, 256, 0, st>>>(tg, reinterpret_cast<double2 *>(W + off[q].vdag), N);
+    k_check_target<<<g1, 256, 0, st>>>(tg, N, 1e-9, bad);
+    launches += 2;
+    if (!off[q].tab.empty() && S[q] > 0) {
+      const long long tot = (long long)S[q] * off[q].tab.size();
+      const int g2 = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, nsm * 16));
+      k_check_gates<<<g2, 256, 0, st>>>(reinterpret_cast<const double *>(W + off[q].gates), S[q],
+                                        (int)off[q].tab.size(),
+                                        reinterpret_cast<const int2 *>(W + off[q].gtab),
+                                        c.var_doubles, 1e-9, bad);
+      launches++;
+    }
+    QF_CHECK(cudaGetLastError());
+    ResProb &P = probs[q];
+    P.n = c.n;
+    P.N = N;
+    P.p = c.p;
+    P.start0 = (int)start0[q];
+    P.S = S[q];
+    P.var_doubles = c.var_doubles;
+    P.gstride = c.var_doubles / 2;
+    P.gd = reinterpret_cast<const GateDesc *>(W + off[q].gd);
+    P.vdag = reinterpret_cast<const double2 *>(W + off[q].vdag);
+    P.cmats = reinterpret_cast<const double2 *>(W + off[q].cm);
+    P.gates = reinterpret_cast<double2 *>(W + off[q].gates);
+  }
+  QF_CHECK(cudaMemcpyAsync(W + o_probs, probs.data(), (size_t)np * sizeof(ResProb),
+                           cudaMemcpyHostToDevice, st));
+  h2d += (long long)np * sizeof(ResProb);
+  int h_bad = 0;
+  QF_CHECK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  QF_CHECK(cudaStreamSynchronize(st));
+  d2h += 4;
+  if (h_bad & 1) {
+    set_error("a target is not unitary to 1e-9 (max-abs of V^dagger V - I)");
+    return QF_E_NOT_UNITARY;
+  }
+  if (h_bad & 2) {
+    set_error("an initial VARIABLE gate is not unitary to 1e-9");
+    return QF_E_NOT_UNITARY;
+  }
+  ResidentArgs A{};
+  A.n = maxn;
+  A.N = 1 << maxn;
+  A.p = 0;
+  A.S = (int)Stot;
+  A.probs = reinterpret_cast<const ResProb *>(W + o_probs);
+  A.nprob = np;
+  A.counter = counter;
+  A.polar_jacobi = 0;
+  A.gather_ltpo_max = 5;
+  A.dist_tol = p.dist_tol;
+  A.diff_tol_a = p.diff_tol_a;
+  A.diff_tol_r = p.diff_tol_r;
+  A.long_diff_r = p.long_diff_r;
+  A.beta = p.beta;
+  A.long_diff_count = p.long_diff_count;
+  A.min_iters = p.min_iters;
+  A.max_iters = p.max_iters;
+  A.reset_iters = p.reset_iters;
+  A.ring = ring;
+  A.hist = reinterpret_cast<double *>(W + o_hist);
+  A.delta = reinterpret_cast<double *>(W + o_delta);
+  A.iters = reinterpret_cast<int *>(W + o_iters);
+  A.verdict = reinterpret_cast<int *>(W + o_verdict);
+  A.R = 0;
+  const int threads = resident_threads(maxn);
+  const size_t smem = (size_t)A.N * A.N * 16 + 8 * 64 * 16;
+  auto kern = maxm == 1 ? k_resident<2, true> : maxm == 2 ? k_resident<4, true> : k_resident<8, true>;
+  QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  const int g = (int)std::max<long long>(1, std::min<long long>(Stot, (long long)std::max(1, per_sm) * nsm));
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (p.profile) {
+    QF_CHECK(cudaEventCreate(&ev[0]));
+    QF_CHECK(cudaEventCreate(&ev[1]));
+    QF_CHECK(cudaEventRecord(ev[0], st));
+  }
+  if (Stot > 0) {
+    kern<<<g, threads, smem, st>>>(A);
+    launches++;
+    QF_CHECK(cudaGetLastError());
+  }
+  float res_ms = 0.f;
+  if (p.profile) {
+    QF_CHECK(cudaEventRecord(ev[1], st));
+    QF_CHECK(cudaEventSynchronize(ev[1]));
+    cudaEventElapsedTime(&res_ms, ev[0], ev[1]);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+  }
+  // ---- a8 per problem: summaries, best start (argmin Delta, ties -> lowest), gates
+  std::vector<double> delta(Stot);
+  std::vector<int> iters(Stot), verdict(Stot);
+  if (Stot > 0) {
+    QF_CHECK(cudaMemcpyAsync(delta.data(), W + o_delta, Stot * 8, cudaMemcpyDeviceToHost, st));
+    QF_CHECK(cudaMemcpyAsync(iters.data(), W + o_iters, Stot * 4, cudaMemcpyDeviceToHost, st));
+    QF_CHECK(cudaMemcpyAsync(verdict.data(), W + o_verdict, Stot * 4, cudaMemcpyDeviceToHost, st));
+    d2h += Stot * 16;
+  }
+  for (int q = 0; q < np; q++) {
+    qf_result_s &r = *outs[q];
+    const qf_circuit_s &c = *cs[q];
+    r.num_starts = S[q];
+    r.var_doubles = c.var_doubles;
+    r.all_gates = true;
+    if (c.var_doubles > 0 && S[q] > 0) {
+      r.gates.resize((size_t)S[q] * c.var_doubles);
+      QF_CHECK(cudaMemcpyAsync(r.gates.data(), W + off[q].gates, r.gates.size() * 8,
+                               cudaMemcpyDeviceToHost, st));
+      d2h += (long long)r.gates.size() * 8;
+    }
+  }
+  QF_CHECK(cudaStreamSynchronize(st));
+  for (int q = 0; q < np; q++) {
+    qf_result_s &r = *outs[q];
+    const qf_circuit_s &c = *cs[q];
+    const int N = 1 << c.n;
+    r.summary.resize(S[q]);
+    int best = -1, mx = 0;
+    long long ss = 0;
+    double step_f = 0.0, init_f = 0.0, f = 0.0;
+    for (int k = 0; k < c.p; k++) {
+      step_f += 2.0 * 16.0 * (1 << c.arity[k]) * (double)N * N;
+      init_f += 8.0 * (1 << c.arity[k]) * (double)N * N;
+    }
+    for (int t = 0; t < S[q]; t++) {
+      const long long gi = start0[q] + t;
+      qf_summary &sm = r.summary[t];
+      sm.delta = delta[gi];
+      sm.iters = iters[gi];
+      sm.verdict = verdict[gi];
+      if (best < 0 || sm.delta < r.summary[best].delta ||
+          (!(r.summary[best].delta == r.summary[best].delta) && sm.delta == sm.delta))
+        best = t;
+      ss += sm.iters;
+      mx = std::max(mx, sm.iters);
+      const int inits = sm.iters >= 1 ? 1 + (sm.iters - 1) / p.reset_iters : 1;
+      f += sm.iters * step_f + inits * init_f;
+    }
+    r.best = best;
+    r.stats.kernel_launches = launches;
+    r.stats.sweeps = mx;
+    r.stats.engine = QF_ENGINE_RESIDENT;
+    r.stats.start_sweeps = ss;
+    r.stats.sweep_flops = f;
+    r.stats.resident_ms = res_ms;  // the whole launch (shared by its problems)
+    r.stats.h2d_bytes = h2d;
+    r.stats.d2h_bytes = d2h;
   }
   return QF_OK;
 }

@@ -91,6 +91,11 @@ struct EngineOut {
   bool host_all_gates = false;          // copy every start's gates to host
 };
 
+// NEXT-2: np problems in one resident launch (host inputs, host results)
+qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *const *targets,
+                          const double *const *initials, const int *S, const qf_params &p,
+                          cudaStream_t st, qf_result_s *const *outs);
+
 qf_status engine_run(const qf_circuit_s &c, const double *d_target,
                      const double *d_initial, const qf_params &p, void *ws,
                      size_t ws_bytes, cudaStream_t st, const EngineOut &out);

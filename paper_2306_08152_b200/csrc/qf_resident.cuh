@@ -34,6 +34,25 @@ struct GateDesc {
 // cached loads); templates with more gates use the streaming engine
 constexpr int kResMaxGates = 240;
 
+// One problem of a multi-problem launch (NEXT-2, qf_instantiate_many): its
+// starts are [start0, start0 + S) of the launch's global start numbering;
+// its tables live in global memory.
+struct ResProb {
+  int n, N, p, start0, S, var_doubles;
+  long long gstride;     // complex per start in `gates`
+  const GateDesc *gd;    // p gate descriptors
+  const double2 *vdag;   // N x N
+  const double2 *cmats;  // CONSTANT gate matrices
+  double2 *gates;        // S x gstride: packed VARIABLE gates
+};
+
+// What a CTA needs of the problem of the start it runs (uniform values)
+struct ResView {
+  int n, N, p;
+  const double2 *vdag, *cmats;
+  double2 *u0;  // this start's packed gates
+};
+
 struct ResidentArgs {
   int n, N, p, S;
   GateDesc gd[kResMaxGates];
@@ -44,6 +63,8 @@ struct ResidentArgs {
   double2 *vstore;    // nullptr: cold Jacobi
   long long vstride;
   int *counter;       // work-stealing start counter (zeroed before launch)
+  const ResProb *probs;  // multi-problem launch: nprob problems, S = sum of starts
+  int nprob;
   int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   double dist_tol, diff_tol_a, diff_tol_r, long_diff_r, beta;
@@ -176,11 +197,11 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
 // per output take r = k, k+TPO, ... ascending; a fixed xor-tree combines them
 // (deterministic, independent of which CTA runs the start).
 template <int D>
-__device__ void res_gather_d(const ResidentArgs &A, const double2 *ct, const GateDesc &g,
-                             double2 *Pm) {
+__device__ void res_gather_d(const ResidentArgs &A, const ResView &V, const double2 *ct,
+                             const GateDesc &g, double2 *Pm) {
   constexpr int DD = D * D;
   constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
-  const int nt = blockDim.x, N = A.N, R = N >> LD;
+  const int nt = blockDim.x, N = V.N, R = N >> LD;
   // threads per output: a power of two in [1, 32] (shifts, no runtime division)
   int ltpo = (31 - __clz(nt)) - 2 * LD;
   ltpo = ltpo < 0 ? 0 : (ltpo > A.gather_ltpo_max ? A.gather_ltpo_max : ltpo);
@@ -194,7 +215,7 @@ __device__ void res_gather_d(const ResidentArgs &A, const double2 *ct, const Gat
     if (o < DD) {
       const int a = o / D, b = o % D;
       for (int r = k; r < R; r += tpo) {
-        const int sp = rspread(g, A.n, r);
+        const int sp = rspread(g, V.n, r);
         const double2 v = ct[sidx(sp | g.abits[a], sp | g.abits[b], N)];
         acc.x += v.x;
         acc.y += v.y;
@@ -210,15 +231,15 @@ __device__ void res_gather_d(const ResidentArgs &A, const double2 *ct, const Gat
 }
 
 template <int MAXD>
-__device__ __forceinline__ void res_gather(const ResidentArgs &A, const double2 *ct,
-                                           const GateDesc &g, double2 *Pm) {
+__device__ __forceinline__ void res_gather(const ResidentArgs &A, const ResView &V,
+                                           const double2 *ct, const GateDesc &g, double2 *Pm) {
   if (g.d == 2) {
-    res_gather_d<2>(A, ct, g, Pm);
+    res_gather_d<2>(A, V, ct, g, Pm);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      res_gather_d<4>(A, ct, g, Pm);
+      res_gather_d<4>(A, V, ct, g, Pm);
     } else if constexpr (MAXD >= 8) {
-      res_gather_d<8>(A, ct, g, Pm);
+      res_gather_d<8>(A, V, ct, g, Pm);
     }
   }
 }
@@ -282,12 +303,12 @@ __device__ void res_update(const ResidentArgs &A, const GateDesc &g, double2 *u,
 // backward L = u_old^H, R = u_new / forward L = u_new, R = u_old^H
 // (P:599-605).  CONSTANT: the fixed matrix and its adjoint.
 template <int D>
-__device__ void res_prepare_d(const ResidentArgs &A, const double2 *ct, const GateDesc &g, int s,
-                              int forward, double2 *Lb, double2 *Rb, double2 *Uo, double2 *Pm,
-                              double2 *Am, double2 *Vm, int lane) {
+__device__ void res_prepare_d(const ResidentArgs &A, const ResView &V, const double2 *ct,
+                              const GateDesc &g, int s, int forward, double2 *Lb, double2 *Rb,
+                              double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm, int lane) {
   constexpr int DD = D * D;
   if (g.kind == 0) {
-    double2 *u = A.gates + (long long)s * A.gstride + g.goff;
+    double2 *u = V.u0 + g.goff;
     double2 *vs = (A.vstore && D > 2)
                       ? A.vstore + (long long)s * A.vstride + g.voff + (forward ? DD : 0)
                       : nullptr;
@@ -299,7 +320,7 @@ __device__ void res_prepare_d(const ResidentArgs &A, const double2 *ct, const Ga
       Rb[e] = forward ? od : Pm[e];
     }
   } else {
-    const double2 *cm = A.cmats + g.goff;
+    const double2 *cm = V.cmats + g.goff;
     for (int e = lane; e < DD; e += 32) {
       const int i = e / D, k = e % D;
       const double2 cd = cconj(cm[k * D + i]);
@@ -311,17 +332,17 @@ __device__ void res_prepare_d(const ResidentArgs &A, const double2 *ct, const Ga
 }
 
 template <int MAXD>
-__device__ __forceinline__ void res_prepare(const ResidentArgs &A, const double2 *ct,
-                                            const GateDesc &g, int s, int forward, double2 *Lb,
-                                            double2 *Rb, double2 *Uo, double2 *Pm, double2 *Am,
-                                            double2 *Vm, int lane) {
+__device__ __forceinline__ void res_prepare(const ResidentArgs &A, const ResView &V,
+                                            const double2 *ct, const GateDesc &g, int s,
+                                            int forward, double2 *Lb, double2 *Rb, double2 *Uo,
+                                            double2 *Pm, double2 *Am, double2 *Vm, int lane) {
   if (g.d == 2) {
-    res_prepare_d<2>(A, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
+    res_prepare_d<2>(A, V, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      res_prepare_d<4>(A, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
+      res_prepare_d<4>(A, V, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
     } else if constexpr (MAXD >= 8) {
-      res_prepare_d<8>(A, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
+      res_prepare_d<8>(A, V, ct, g, s, forward, Lb, Rb, Uo, Pm, Am, Vm, lane);
     }
   }
 }
@@ -330,50 +351,50 @@ __device__ __forceinline__ void res_prepare(const ResidentArgs &A, const double2
 // res_sandwich_blocks.  d = 8 (two-phase, internal barriers) only with mode 0
 // and all threads.
 template <int MAXD>
-__device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResidentArgs &A,
+__device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResView &V,
                                           const double2 *Lb, const double2 *Rb, int mode, int dm,
                                           int t0, int nt) {
   if (g.d == 2) {
-    res_sandwich_blocks<2>(ct, g, A.n, A.N, Lb, Rb, mode, dm, t0, nt);
+    res_sandwich_blocks<2>(ct, g, V.n, V.N, Lb, Rb, mode, dm, t0, nt);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      res_sandwich_blocks<4>(ct, g, A.n, A.N, Lb, Rb, mode, dm, t0, nt);
+      res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, mode, dm, t0, nt);
     } else if constexpr (MAXD >= 8) {
-      res_sandwich<8>(ct, g, A.n, A.N, Lb, Rb);
+      res_sandwich<8>(ct, g, V.n, V.N, Lb, Rb);
     }
   }
 }
 
 template <int D>
-__device__ void res_apply_left(double2 *ct, const GateDesc &g, const ResidentArgs &A,
+__device__ void res_apply_left(double2 *ct, const GateDesc &g, const ResView &V,
                                const double2 *src, double2 *Ls) {
   for (int e = threadIdx.x; e < D * D; e += blockDim.x) Ls[e] = src[e];
   __syncthreads();
-  res_sandwich<D>(ct, g, A.n, A.N, Ls, nullptr);
+  res_sandwich<D>(ct, g, V.n, V.N, Ls, nullptr);
 }
 
 template <int MAXD>
-__device__ void res_init(const ResidentArgs &A, double2 *ct, const GateDesc *gdesc, int s,
-                         double2 *Ls) {
-  const int NN = A.N * A.N;
+__device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
+                         const GateDesc *gdesc, int s, double2 *Ls) {
+  const int NN = V.N * V.N;
   for (int e = threadIdx.x; e < NN; e += blockDim.x)
-    ct[sidx(e >> A.n, e & (A.N - 1), A.N)] = A.vdag[e];
+    ct[sidx(e >> V.n, e & (V.N - 1), V.N)] = V.vdag[e];
   __syncthreads();
-  for (int k = 0; k < A.p; k++) {
+  for (int k = 0; k < V.p; k++) {
     const GateDesc &g = gdesc[k];
-    const double2 *src = g.kind == 0 ? A.gates + (long long)s * A.gstride + g.goff : A.cmats + g.goff;
+    const double2 *src = g.kind == 0 ? V.u0 + g.goff : V.cmats + g.goff;
     if (g.d == 2) {
-      res_apply_left<2>(ct, g, A, src, Ls);
+      res_apply_left<2>(ct, g, V, src, Ls);
     } else if constexpr (MAXD >= 4) {
       if (g.d == 4) {
-        res_apply_left<4>(ct, g, A, src, Ls);
+        res_apply_left<4>(ct, g, V, src, Ls);
       } else if constexpr (MAXD >= 8) {
-        res_apply_left<8>(ct, g, A, src, Ls);
+        res_apply_left<8>(ct, g, V, src, Ls);
       }
     }
   }
   if (A.vstore) {  // warm starts restart from I with every (re)build
-    for (int k = 0; k < A.p; k++) {
+    for (int k = 0; k < V.p; k++) {
       const GateDesc &g = gdesc[k];
       if (g.kind != 0) continue;
       double2 *v = A.vstore + (long long)s * A.vstride + g.voff;
@@ -399,35 +420,62 @@ __device__ __forceinline__ int rest_bits_in(const GateDesc &g, int n, int next_m
 // j >= p -> (gate j-p, forward).  Step j's operands live in buffer j & 1.
 // (Overlapping the next gate's polar factor with this sandwich on the other
 // warps was measured slower at 3 CTAs per SM and is not used.)
-template <int MAXD>
+// MULTI: the launch holds several problems (NEXT-2): each start finds its
+// problem in A.probs (gate tables in global memory); otherwise the single
+// problem's gate table is read from the kernel parameters.
+template <int MAXD, bool MULTI>
 __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ ResidentArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   double2 *ct = reinterpret_cast<double2 *>(smraw);
-  double2 *Lb = ct + A.N * A.N;  // [2][64]
+  double2 *Lb = ct + A.N * A.N;  // [2][64]; A.N = the largest N of the launch
   double2 *Rb = Lb + 128;        // [2][64]
   double2 *Uo = Rb + 128;
   double2 *Pm = Uo + 64;
   double2 *Am = Pm + 64;
   double2 *Vm = Am + 64;
-  const GateDesc *gdesc = A.gd;  // kernel parameters (constant bank)
+  const GateDesc *gdesc = A.gd;  // kernel parameters (constant bank); MULTI: per problem
   __shared__ int s_start, s_verdict;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int steps = 2 * A.p;
   // the serial work (environment, polar factor, cost) runs on warp sw0 (warp 0;
   // the last warp measured the same)
   const int sw0 = 0;
   const bool serial = tid >= sw0 && tid < sw0 + 32;
   const int lane = tid - sw0;
-  auto gate_of = [&](int j, int &fw) {
-    fw = j >= A.p;
-    return fw ? j - A.p : A.p - 1 - j;
-  };
   for (;;) {
     if (tid == 0) s_start = atomicAdd(A.counter, 1);
     __syncthreads();
     const int s = s_start;
     if (s >= A.S) break;
-    res_init<MAXD>(A, ct, gdesc, s, Lb);
+    ResView V;
+    if constexpr (MULTI) {
+      int lo = 0, hi = A.nprob - 1;  // last problem with start0 <= s
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (A.probs[mid].start0 <= s) lo = mid;
+        else hi = mid - 1;
+      }
+      const ResProb &P = A.probs[lo];
+      V.n = P.n;
+      V.N = P.N;
+      V.p = P.p;
+      V.vdag = P.vdag;
+      V.cmats = P.cmats;
+      V.u0 = P.gates + (long long)(s - P.start0) * P.gstride;
+      gdesc = P.gd;  // global memory
+    } else {
+      V.n = A.n;
+      V.N = A.N;
+      V.p = A.p;
+      V.vdag = A.vdag;
+      V.cmats = A.cmats;
+      V.u0 = A.gates + (long long)s * A.gstride;
+    }
+    const int steps = 2 * V.p;
+    auto gate_of = [&](int j, int &fw) {
+      fw = j >= V.p;
+      return fw ? j - V.p : V.p - 1 - j;
+    };
+    res_init<MAXD>(A, V, ct, gdesc, s, Lb);
     int it = 0;
     // operands of step j2 into buffer (j2 & 1): all threads gather the
     // environment (VARIABLE gates), the serial warp stages u_old (prefetched
@@ -442,12 +490,12 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
 #ifdef QF_POLAR_COUNT
         const long long tg0 = clock64();
 #endif
-        res_gather<MAXD>(A, ct, g2, Pm);
+        res_gather<MAXD>(A, V, ct, g2, Pm);
 #ifdef QF_POLAR_COUNT
         if (tid == 0) atomicAdd(&qf_t_gather, (unsigned long long)(clock64() - tg0));
 #endif
         if (serial) {
-          const double2 *u2 = A.gates + (long long)s * A.gstride + g2.goff;
+          const double2 *u2 = V.u0 + g2.goff;
 #pragma unroll
           for (int q = 0; q < 2; q++) {
             const int e = lane + 32 * q;
@@ -456,7 +504,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
         }
         __syncthreads();
       }
-      if (serial) res_prepare<MAXD>(A, ct, g2, s, fw2, Lb + off, Rb + off, Uo, Pm, Am, Vm, lane);
+      if (serial) res_prepare<MAXD>(A, V, ct, g2, s, fw2, Lb + off, Rb + off, Uo, Pm, Am, Vm, lane);
       __syncthreads();
     };
     if (A.max_iters > 0) prepare(0, false);
@@ -471,7 +519,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
             int fw2;                 // hidden behind this sandwich)
             const GateDesc &g2 = gdesc[gate_of(j + 1, fw2)];
             if (g2.kind == 0) {
-              const double2 *u2 = A.gates + (long long)s * A.gstride + g2.goff;
+              const double2 *u2 = V.u0 + g2.goff;
 #pragma unroll
               for (int q = 0; q < 2; q++) {
                 const int e = lane + 32 * q;
@@ -482,7 +530,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
 #ifdef QF_POLAR_COUNT
           const long long c0 = clock64();
 #endif
-          res_apply<MAXD>(ct, g, A, Lb + buf, Rb + buf, 0, 0, tid, nt);
+          res_apply<MAXD>(ct, g, V, Lb + buf, Rb + buf, 0, 0, tid, nt);
           __syncthreads();
 #ifdef QF_POLAR_COUNT
           const long long c1 = clock64();
@@ -501,15 +549,15 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
       // cost + termination, warp 0
       if (serial) {
         double re = 0.0, im = 0.0;
-        for (int i = lane; i < A.N; i += 32) {
-          re += ct[sidx(i, i, A.N)].x;
-          im += ct[sidx(i, i, A.N)].y;
+        for (int i = lane; i < V.N; i += 32) {
+          re += ct[sidx(i, i, V.N)].x;
+          im += ct[sidx(i, i, V.N)].y;
         }
         for (int off = 1; off < 32; off <<= 1) {
           re += __shfl_xor_sync(0xffffffffu, re, off);
           im += __shfl_xor_sync(0xffffffffu, im, off);
         }
-        const double c = 1.0 - hypot(re, im) / (double)A.N;
+        const double c = 1.0 - hypot(re, im) / (double)V.N;
         if (lane == 0) {
           int v = 0;
           if (it == 0) {
@@ -544,7 +592,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
           const int slot = A.rec_slot[s];
           if (slot >= 0) {
             if (lane == 0) A.rec_cost[(long long)slot * A.R + it - 1] = c;
-            const double *gsrc = reinterpret_cast<const double *>(A.gates + (long long)s * A.gstride);
+            const double *gsrc = reinterpret_cast<const double *>(V.u0);
             double *dst = A.rec_gates + ((long long)slot * A.R + it - 1) * A.var_doubles;
             for (int e = lane; e < A.var_doubles; e += 32) dst[e] = gsrc[e];
           }
@@ -552,7 +600,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
       }
       __syncthreads();
       if (s_verdict != 0) break;
-      if (it % A.reset_iters == 0) res_init<MAXD>(A, ct, gdesc, s, Lb);
+      if (it % A.reset_iters == 0) res_init<MAXD>(A, V, ct, gdesc, s, Lb);
       prepare(0, false);  // operands of the next sweep's first step
     }
     __syncthreads();

@@ -108,3 +108,20 @@ def test_select_best_host():
     assert qf.qf_select_best_host(s) == 2
     s["delta"] = np.nan
     assert qf.qf_select_best_host(s) == 0
+
+
+def test_instantiate_many_validation_precedes_device():
+    w = qfgen.workload("C1")
+    c = qf.Circuit.from_workload(w)
+    big = qf.Circuit(7, [(0, 1)], [qfgen.VARIABLE], [None])
+    rng = np.random.default_rng(0)
+    cases = [
+        (([c, big], [w.target_unitary(), np.eye(128)], [w.initial(), rng.standard_normal((2, 32))]), {}),
+        (([c], [w.target_unitary()], [w.initial()]), {"batch_policy": qf.QF_BATCH_PAPER}),
+        (([c], [w.target_unitary()], [w.initial()]), {"engine": qf.QF_ENGINE_STREAM}),
+        (([c], [w.target_unitary()], [w.initial()]), {"beta": 2.0}),
+    ]
+    for args, kw in cases:
+        with pytest.raises(qf.QfError) as e:
+            qf.qf_instantiate_many(*args, **kw)
+        assert e.value.status == qf.QF_E_ARG
