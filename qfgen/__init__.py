@@ -269,6 +269,19 @@ def workload(name: str) -> Workload:
 ALL = ["C1", "C2", "C3", "C4", "C5", "C2+", "C3+"]
 
 
+def many_workload(count=1024, starts=32, max_iters=1000):
+    """NEXT-2 workload: `count` independent
+    3-qubit blocks, the shape partitioning produces; block q is a ladder of
+    4 + (q mod 7) VARIABLE U(4) gates re-instantiated to its own unitary
+    (self-target, seeds 1100 + q / 2100 + q), 32 multistarts each."""
+    out = []
+    for q in range(count):
+        l, k, c = _ladder(3, 4 + q % 7)
+        out.append(Workload(f"B{q}", 3, l, k, c, starts, max_iters, "self", 100 + q,
+                            f"3-qubit block {q}: ladder of {len(l)} VAR U(4), self-target"))
+    return out
+
+
 def random_template(n, p, arities=(1, 2, 3), seed=0, const_frac=0.0):
     """A random template for tests: random arity, random distinct, randomly
     ordered locations; a fraction of CONSTANT gates (Haar matrices)."""
