@@ -54,7 +54,13 @@ typedef enum {
   QF_E_NCCL = 7          /* reserved: collectives run in the binding layer */
 } qf_status;
 
-typedef enum { QF_GATE_VARIABLE = 0, QF_GATE_CONSTANT = 1 } qf_gate_kind;
+/* Gate kinds.  VARIABLE: a general U(2^m), updated by the SVD (polar)
+ * step.  CONSTANT: a fixed matrix, moved across but never
+ * updated (reading R14).  RZ (NEXT-4): the 1-qubit R_z(theta) =
+ * diag(1, e^{i theta}) of Sec. 3.1.3, updated analytically to
+ * theta = -arg M_11 (reading R19); stored in the packed gates as
+ * its 2 x 2 matrix, which must have that form (1e-9). */
+typedef enum { QF_GATE_VARIABLE = 0, QF_GATE_CONSTANT = 1, QF_GATE_RZ = 2 } qf_gate_kind;
 
 /* Per-start verdicts (precedence DESIGN.md reading R17). */
 typedef enum {
@@ -194,6 +200,15 @@ qf_status qf_instantiate_many(int32_t num_problems, const qf_circuit_t *circuits
                               const double *const *targets, const double *const *initials,
                               const int32_t *num_starts, const qf_params *p,
                               qf_result_t *out);
+
+/* NEXT-4: ZYZ / U3 angles of a 2 x 2 unitary u (interleaved
+ * complex, row-major): out = (theta, phi, lambda, gamma) with
+ * u = e^{i gamma} U3(theta, phi, lambda),
+ * U3 = [[cos(t/2), -e^{i l} sin(t/2)], [e^{i p} sin(t/2), e^{i(p+l)} cos(t/2)]],
+ * theta in [0, pi], phi, lambda, gamma in (-pi, pi]; lambda = 0 where the
+ * decomposition is not unique (theta = 0 or pi).  Host-only, no device.
+ * Errors: QF_E_ARG (NULL), QF_E_NOT_UNITARY (> 1e-9). */
+qf_status qf_unitary_to_u3(const double *u, double *out);
 
 /* Device workspace, in bytes, that qf_instantiate_device needs. */
 size_t qf_workspace_size(qf_circuit_t c, const qf_params *p);

@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "qf_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-VARIABLE, CONSTANT = 0, 1
+VARIABLE, CONSTANT, RZ = 0, 1, 2
 RUNNING, CONVERGED, PLATEAU_SHORT, PLATEAU_LONG, MAX_ITER, NUMERIC_FAIL, BATCH_STOPPED = range(7)
 
 
@@ -88,6 +88,7 @@ def _declare(L):
     L.oracle_svd.argtypes = [ctypes.c_int, _D, _D, _D, _D]
     L.oracle_svd.restype = ctypes.c_int
     L.oracle_optimize_gate.argtypes = [ctypes.c_int, _D, _D, ctypes.c_double, _D, _D]
+    L.oracle_optimize_rz.argtypes = [_D, _D, ctypes.c_double, _D]
     L.oracle_init_ct.argtypes = [ctypes.POINTER(_Circuit), _D, _D, _D]
     L.oracle_sweep.argtypes = [ctypes.POINTER(_Circuit), _D, _D, ctypes.c_double, _D]
     L.oracle_terminate.argtypes = [ctypes.POINTER(Params), ctypes.c_int, _D]
@@ -148,7 +149,7 @@ class Circuit:
 
     @property
     def var_doubles(self) -> int:
-        return sum(2 * 4 ** len(l) for l, k in zip(self.locs, self.kinds) if k == VARIABLE)
+        return sum(2 * 4 ** len(l) for l, k in zip(self.locs, self.kinds) if k != CONSTANT)
 
 
 # ---------------------------------------------------------------- blocks
@@ -203,6 +204,13 @@ def optimize_gate(E: np.ndarray, u_old: np.ndarray, beta: float = 0.0):
     lib().oracle_optimize_gate(d, _dp(_cplx(E)), _dp(_cplx(u_old)), float(beta),
                                _dp(out.view(np.float64)), _dp(ss))
     return out, float(ss[0])
+
+
+def optimize_rz(E: np.ndarray, u_old: np.ndarray, beta: float = 0.0):
+    """R_z(theta) update of a 2 x 2 environment (reading R19)."""
+    out = np.zeros((2, 2), dtype=np.complex128)
+    lib().oracle_optimize_rz(_dp(_cplx(E)), _dp(_cplx(u_old)), float(beta), _dp(out.view(np.float64)))
+    return out
 
 
 def init_ct(circ: Circuit, target: np.ndarray, gates: np.ndarray) -> np.ndarray:

@@ -302,6 +302,21 @@ void oracle_optimize_gate(int d, const double *env, const double *u_old,
   free(D);
 }
 
+void oracle_optimize_rz(const double *env, const double *u_old, double beta, double *u_new) {
+  /* M_11 = (1 - beta) E_11 + beta conj(u_old_11) */
+  const cx m11 = cx_add(cx_scale(mget(env, 2, 1, 1), 1.0 - beta),
+                        cx_scale(cx_conj(mget(u_old, 2, 1, 1)), beta));
+  if (m11.re == 0.0 && m11.im == 0.0) {
+    memcpy(u_new, u_old, sizeof(double) * 8);
+    return;
+  }
+  const double theta = -atan2(m11.im, m11.re);
+  mset(u_new, 2, 0, 0, cx_make(1.0, 0.0));
+  mset(u_new, 2, 0, 1, cx_make(0.0, 0.0));
+  mset(u_new, 2, 1, 0, cx_make(0.0, 0.0));
+  mset(u_new, 2, 1, 1, cx_make(cos(theta), sin(theta)));
+}
+
 /* ------------------------------------------------------------------ */
 /* template helpers                                                    */
 /* ------------------------------------------------------------------ */
@@ -316,19 +331,19 @@ static const double *gate_matrix(const oracle_circuit *c, const double *gates,
   int var_off = 0, const_off = 0;
   for (int j = 0; j < k; j++) {
     const int dd = 1 << (2 * c->arity[j]);
-    if (c->kind[j] == ORACLE_VARIABLE)
+    if (c->kind[j] != ORACLE_CONSTANT)
       var_off += 2 * dd;
     else
       const_off += 2 * dd;
   }
-  return c->kind[k] == ORACLE_VARIABLE ? gates + var_off
+  return c->kind[k] != ORACLE_CONSTANT ? gates + var_off
                                        : c->const_mats + const_off;
 }
 
 int oracle_var_doubles(const oracle_circuit *c) {
   int s = 0;
   for (int k = 0; k < c->p; k++)
-    if (c->kind[k] == ORACLE_VARIABLE) s += 2 << (2 * c->arity[k]);
+    if (c->kind[k] != ORACLE_CONSTANT) s += 2 << (2 * c->arity[k]);
   return s;
 }
 
@@ -356,9 +371,12 @@ void oracle_sweep(const oracle_circuit *c, double *ct, double *gates,
     const int *loc = c->loc + loc_offset(c, k);
     double *u = (double *)gate_matrix(c, gates, k);
     oracle_apply_left(n, m, loc, u, 1, ct); /* ApplyRight(inverse=True) */
-    if (c->kind[k] == ORACLE_VARIABLE) {
-      oracle_env(n, m, loc, ct, env);                  /* CalcEnvMat */
-      oracle_optimize_gate(d, env, u, beta, unew, 0);  /* OptimizeGate */
+    if (c->kind[k] != ORACLE_CONSTANT) {
+      oracle_env(n, m, loc, ct, env); /* CalcEnvMat */
+      if (c->kind[k] == ORACLE_RZ)
+        oracle_optimize_rz(env, u, beta, unew);
+      else
+        oracle_optimize_gate(d, env, u, beta, unew, 0); /* OptimizeGate */
       memcpy(u, unew, sizeof(double) * 2 * d * d);
     }
     oracle_apply_right(n, m, loc, u, 0, ct); /* ApplyLeft(u_opt) */
@@ -370,9 +388,12 @@ void oracle_sweep(const oracle_circuit *c, double *ct, double *gates,
     const int *loc = c->loc + loc_offset(c, k);
     double *u = (double *)gate_matrix(c, gates, k);
     oracle_apply_right(n, m, loc, u, 1, ct); /* ApplyLeft(inverse=True) */
-    if (c->kind[k] == ORACLE_VARIABLE) {
+    if (c->kind[k] != ORACLE_CONSTANT) {
       oracle_env(n, m, loc, ct, env);
-      oracle_optimize_gate(d, env, u, beta, unew, 0);
+      if (c->kind[k] == ORACLE_RZ)
+        oracle_optimize_rz(env, u, beta, unew);
+      else
+        oracle_optimize_gate(d, env, u, beta, unew, 0);
       memcpy(u, unew, sizeof(double) * 2 * d * d);
     }
     oracle_apply_left(n, m, loc, u, 0, ct); /* ApplyRight(u_opt) */

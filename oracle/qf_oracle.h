@@ -29,7 +29,9 @@
 extern "C" {
 #endif
 
-enum { ORACLE_VARIABLE = 0, ORACLE_CONSTANT = 1 };
+/* RZ: the parameterised R_z(theta) = diag(1, e^{i theta}) of Sec. 3.1.3
+ * (P:549-556), 1 qubit, stored like a VARIABLE gate (its 2 x 2 matrix). */
+enum { ORACLE_VARIABLE = 0, ORACLE_CONSTANT = 1, ORACLE_RZ = 2 };
 enum {
   ORACLE_RUNNING = 0,
   ORACLE_CONVERGED = 1,
@@ -90,6 +92,11 @@ void oracle_init_ct(const oracle_circuit *c, const double *target,
  * entries, in update order. */
 void oracle_sweep(const oracle_circuit *c, double *ct, double *gates,
                   double beta, double *trace_log);
+/* R_z update (reading R19): with M = (1-beta) env + beta
+ * u_old^dagger, Re Tr(M R_z(theta)) = Re M_00 + Re(M_11 e^{i theta}), maximal
+ * at theta = -arg M_11; u_new = diag(1, e^{i theta}).  M_11 = 0: u_old kept. */
+void oracle_optimize_rz(const double *env, const double *u_old, double beta, double *u_new);
+
 /* Termination test after sweep `it` (1-based) given costs c[1..it]
  * (c[0] unused).  Returns ORACLE_RUNNING or a verdict. */
 int oracle_terminate(const oracle_params *prm, int it, const double *c);

@@ -20,7 +20,7 @@ import numpy as np
 from . import _build
 
 QF_OK, QF_E_ARG, QF_E_DIM, QF_E_LOCATION, QF_E_NOT_UNITARY, QF_E_OOM, QF_E_CUDA, QF_E_NCCL = range(8)
-QF_GATE_VARIABLE, QF_GATE_CONSTANT = 0, 1
+QF_GATE_VARIABLE, QF_GATE_CONSTANT, QF_GATE_RZ = 0, 1, 2
 (QF_RUNNING, QF_CONVERGED, QF_PLATEAU_SHORT, QF_PLATEAU_LONG, QF_MAX_ITER, QF_NUMERIC_FAIL,
  QF_BATCH_STOPPED) = range(7)
 QF_ENGINE_AUTO, QF_ENGINE_STREAM, QF_ENGINE_RESIDENT = range(3)
@@ -35,7 +35,7 @@ EXPORTS = [
     "qf_circuit_num_qubits", "qf_instantiate", "qf_workspace_size", "qf_instantiate_device",
     "qf_result_get", "qf_result_best", "qf_result_num_starts", "qf_result_trace",
     "qf_result_stats", "qf_result_destroy", "qf_select_best_device", "qf_select_best_host",
-    "qf_last_error", "qf_version", "qf_instantiate_many",
+    "qf_last_error", "qf_version", "qf_instantiate_many", "qf_unitary_to_u3",
 ]
 
 
@@ -146,6 +146,7 @@ def _declare(L):
     L.qf_select_best_host.argtypes = [c.POINTER(qf_summary), c.c_int64, c.POINTER(c.c_int64)]
     L.qf_instantiate_many.argtypes = [c.c_int32, c.POINTER(_VP), c.POINTER(_D), c.POINTER(_D),
                                       _I, c.POINTER(qf_params), c.POINTER(_VP)]
+    L.qf_unitary_to_u3.argtypes = [_D, _D]
     L.qf_last_error.restype = c.c_char_p
     L.qf_last_error.argtypes = []
     L.qf_version.restype = c.c_char_p
@@ -324,6 +325,17 @@ def qf_instantiate_many(circuits, targets, initials, **params) -> list:
 
 
 instantiate_many = qf_instantiate_many
+
+
+def qf_unitary_to_u3(u) -> tuple:
+    """(theta, phi, lambda, gamma) with u = e^{i gamma} U3(theta, phi, lambda)."""
+    a = _cplx(np.asarray(u).reshape(2, 2))
+    out = np.zeros(4)
+    _check(lib().qf_unitary_to_u3(a.ctypes.data_as(_D), out.ctypes.data_as(_D)))
+    return tuple(float(x) for x in out)
+
+
+unitary_to_u3 = qf_unitary_to_u3
 
 
 def qf_workspace_size(circ: Circuit, S, **params) -> int:

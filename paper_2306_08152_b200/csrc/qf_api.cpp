@@ -234,8 +234,12 @@ qf_status qf_circuit_create(int num_qubits, int num_gates, const int *arity,
     c->loc_off.push_back(off);
     off += m;
     const int dd = 1 << (2 * m);
-    if (kinds[k] == QF_GATE_VARIABLE) {
-      c->kind.push_back(QF_GATE_VARIABLE);
+    if (kinds[k] == QF_GATE_VARIABLE || kinds[k] == QF_GATE_RZ) {
+      if (kinds[k] == QF_GATE_RZ && m != 1) {
+        delete c;
+        return fail(QF_E_ARG, "gate " + std::to_string(k) + ": an RZ gate acts on one qubit");
+      }
+      c->kind.push_back(kinds[k]);
       c->var_off.push_back(voff);
       c->const_off.push_back(-1);
       voff += 2 * dd;
@@ -463,6 +467,38 @@ qf_status qf_instantiate_many(int32_t num_problems, const qf_circuit_t *circuits
     return s;
   }
   for (int q = 0; q < num_problems; q++) out[q] = res[q];
+  return QF_OK;
+}
+
+qf_status qf_unitary_to_u3(const double *u, double *out) {
+  qf::g_err.clear();
+  if (!u || !out) return fail(QF_E_ARG, "u and out must not be NULL");
+  if (!(unitarity_error(u, 2) <= 1e-9)) return fail(QF_E_NOT_UNITARY, "u is not unitary to 1e-9");
+  const double a00 = std::hypot(u[0], u[1]), a10 = std::hypot(u[4], u[5]);
+  const double theta = 2.0 * std::atan2(a10, a00);
+  const double eps = 1e-12;
+  double gamma, phi, lam;
+  auto wrap = [](double x) {  // into (-pi, pi]
+    x = std::remainder(x, 2.0 * M_PI);
+    return x <= -M_PI ? x + 2.0 * M_PI : x;
+  };
+  if (a10 <= eps) {  // theta = 0: u = e^{i g} diag(1, e^{i (p + l)})
+    gamma = std::atan2(u[1], u[0]);
+    lam = 0.0;
+    phi = std::atan2(u[7], u[6]) - gamma;
+  } else if (a00 <= eps) {  // theta = pi: u = e^{i g} [[0, -e^{i l}], [e^{i p}, 0]]
+    lam = 0.0;
+    gamma = std::atan2(-u[3], -u[2]);
+    phi = std::atan2(u[5], u[4]) - gamma;
+  } else {
+    gamma = std::atan2(u[1], u[0]);
+    phi = std::atan2(u[5], u[4]) - gamma;
+    lam = std::atan2(-u[3], -u[2]) - gamma;
+  }
+  out[0] = theta;
+  out[1] = wrap(phi);
+  out[2] = wrap(lam);
+  out[3] = wrap(gamma);
   return QF_OK;
 }
 

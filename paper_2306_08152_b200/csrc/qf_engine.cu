@@ -115,9 +115,12 @@ __global__ void k_check_gates(const double *G, long long S, int nvar, const int2
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long s = e / nvar;
-    const int2 g = tab[e % nvar];  // (offset in doubles, d)
+    const int2 g = tab[e % nvar];  // (offset in doubles, d); d < 0: RZ gate of size -d
     const double2 *u = reinterpret_cast<const double2 *>(G + s * var_doubles + g.x);
-    const int d = g.y;
+    const int d = g.y < 0 ? -g.y : g.y;
+    if (g.y < 0 && !(fabs(u[0].x - 1.0) <= tol && fabs(u[0].y) <= tol && fabs(u[1].x) <= tol &&
+                     fabs(u[1].y) <= tol && fabs(u[2].x) <= tol && fabs(u[2].y) <= tol))
+      atomicOr(bad, 2);
     double worst = 0.0;
     for (int i = 0; i < d; i++)
       for (int j = 0; j < d; j++) {
@@ -261,7 +264,7 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
   L.vstride = 0;
   L.nvslots = 0;
   for (int k = 0; k < c.p; k++)
-    if (c.kind[k] == QF_GATE_VARIABLE) {
+    if (c.kind[k] != QF_GATE_CONSTANT) {
       L.vstride += 2LL << (2 * c.arity[k]);
       L.nvslots += 2;
     }
@@ -378,7 +381,7 @@ struct Engine {
     voff.assign(c.p, -1);
     long long o = 0;
     for (int k = 0; k < c.p; k++)
-      if (c.kind[k] == QF_GATE_VARIABLE) {
+      if (c.kind[k] != QF_GATE_CONSTANT) {
         voff[k] = (int)o;
         o += 2LL << (2 * c.arity[k]);
       }
@@ -568,6 +571,7 @@ struct Engine {
     A.forward = forward;
     A.beta = p.beta;
     A.polar_jacobi = polar_jacobi ? 1 : 0;
+    A.rz = c.kind[k] == QF_GATE_RZ ? 1 : 0;
     if (warm) {
       A.vstore = reinterpret_cast<double2 *>(ws + L.vstore);
       A.vstride = L.vstride;
@@ -589,7 +593,7 @@ struct Engine {
   // operand descriptors: the per-start VARIABLE gate, the u_old scratch, or a
   // CONSTANT matrix shared by all starts (stride 0)
   void gate_operand(int k, const double2 *&src, long long &stride) const {
-    if (c.kind[k] == QF_GATE_VARIABLE) {
+    if (c.kind[k] != QF_GATE_CONSTANT) {
       src = reinterpret_cast<const double2 *>(gates()) + c.var_off[k] / 2;
       stride = c.var_doubles / 2;
     } else {
@@ -598,7 +602,7 @@ struct Engine {
     }
   }
   void old_operand(int k, const double2 *&src, long long &stride) const {
-    if (c.kind[k] == QF_GATE_VARIABLE) {
+    if (c.kind[k] != QF_GATE_CONSTANT) {
       src = scratch();
       stride = kScratch;
     } else {
@@ -619,7 +623,7 @@ struct Engine {
   // one gate step of TwoSidedSweep (P:599-605 backward, P:610-616 forward)
   cudaError_t step(int k, int forward) {
     cudaError_t e = cudaSuccess;
-    if (c.kind[k] == QF_GATE_VARIABLE && (e = env(k, forward)) != cudaSuccess) return e;
+    if (c.kind[k] != QF_GATE_CONSTANT && (e = env(k, forward)) != cudaSuccess) return e;
     SandwichArgs A = base_args(k);
     // the schedule's next step: backward k-1 ... 0, then forward 0 ... p-1,
     // then (after the cost) the next sweep's backward p-1
@@ -631,7 +635,7 @@ struct Engine {
       nk = k < c.p - 1 ? k + 1 : c.p - 1;
       nd = k < c.p - 1 ? 1 : 0;
     }
-    next_k = c.kind[nk] == QF_GATE_VARIABLE ? nk : -1;
+    next_k = c.kind[nk] != QF_GATE_CONSTANT ? nk : -1;
     next_dir = nd;
     next_trace = forward && k == c.p - 1;
     if (!forward) {  // ct <- E(u_old)^dagger ct E(u_new)
@@ -669,7 +673,7 @@ struct Engine {
       A.ldag = 0;
       A.rsrc = nullptr;
       // the last pass produces the inputs of the first sweep step (backward p-1)
-      next_k = (k == c.p - 1 && c.kind[k] == QF_GATE_VARIABLE) ? k : -1;
+      next_k = (k == c.p - 1 && c.kind[k] != QF_GATE_CONSTANT) ? k : -1;
       next_dir = 0;
       next_trace = false;
       e = sandwich(A);
@@ -735,10 +739,10 @@ std::vector<GateDesc> make_gdesc(const qf_circuit_s &c, const std::vector<int> *
     GateDesc &g = gd[k];
     g.m = b.m;
     g.d = b.d;
-    g.kind = c.kind[k] == QF_GATE_VARIABLE ? 0 : 1;
-    g.goff = g.kind == 0 ? c.var_off[k] / 2 : c.const_off[k] / 2;
+    g.kind = c.kind[k] == QF_GATE_CONSTANT ? 1 : (c.kind[k] == QF_GATE_RZ ? 2 : 0);
+    g.goff = g.kind != 1 ? c.var_off[k] / 2 : c.const_off[k] / 2;
     g.mask = b.abits[b.d - 1];
-    g.voff = voff && g.kind == 0 ? (*voff)[k] : 0;
+    g.voff = voff && g.kind != 1 ? (*voff)[k] : 0;
     for (int a = 0; a < 8; a++) g.abits[a] = a < b.d ? b.abits[a] : 0;
     for (int q = 0; q < kMaxQubits; q++) g.rest_pos[q] = q < c.n - b.m ? b.rest_pos[q] : 0;
   }
@@ -775,7 +779,8 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   }
   std::vector<int2> tab;
   for (int k = 0; k < c.p; k++)
-    if (c.kind[k] == QF_GATE_VARIABLE) tab.push_back(make_int2(c.var_off[k], 1 << c.arity[k]));
+    if (c.kind[k] != QF_GATE_CONSTANT)  // d < 0: RZ, also check the diag(1, e^{i theta}) form
+      tab.push_back(make_int2(c.var_off[k], c.kind[k] == QF_GATE_RZ ? -2 : 1 << c.arity[k]));
   if (!tab.empty()) {
     QF_CHECK(cudaMemcpyAsync(W + E.L.gtab, tab.data(), tab.size() * sizeof(int2),
                              cudaMemcpyHostToDevice, st));
@@ -783,7 +788,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   }
   std::vector<int2> vslots;
   for (int k = 0; k < c.p; k++)
-    if (c.kind[k] == QF_GATE_VARIABLE) {
+    if (c.kind[k] != QF_GATE_CONSTANT) {
       const int d = 1 << c.arity[k];
       vslots.push_back(make_int2(E.voff[k], d));
       vslots.push_back(make_int2(E.voff[k] + d * d, d));
@@ -1138,7 +1143,8 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
     const size_t N = (size_t)1 << c.n;
     off[q].desc = make_gdesc(c, nullptr);
     for (int k = 0; k < c.p; k++)
-      if (c.kind[k] == QF_GATE_VARIABLE) off[q].tab.push_back(make_int2(c.var_off[k], 1 << c.arity[k]));
+      if (c.kind[k] != QF_GATE_CONSTANT)
+        off[q].tab.push_back(make_int2(c.var_off[k], c.kind[k] == QF_GATE_RZ ? -2 : 1 << c.arity[k]));
     off[q].tgt = take(N * N * 16);
     off[q].vdag = take(N * N * 16);
     off[q].cm = take(c.const_mats.size() * 8);

@@ -233,6 +233,7 @@ struct EnvArgs {
   long long vstride;    // complex per start
   int voff;             // complex offset of (gate, direction)
   int polar_jacobi;     // 1: one-sided Jacobi instead of Newton-Schulz
+  int rz;               // 1: R_z gate (analytic update, d = 2)
 };
 
 // Round-robin (circle method) pairing for a parallel-ordered Jacobi sweep:
@@ -641,6 +642,22 @@ __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U,
   return done;
 }
 
+// R_z(theta) = diag(1, e^{i theta}) update (reading R19): with
+// A = M^dagger (M = (1 - beta) E + beta u_old^dagger, as formed for the polar
+// factor), Re Tr(M R_z) is maximal at e^{i theta} = A_11 / |A_11|; A_11 = 0
+// keeps u_old.  One warp; result in U (2 x 2).
+__device__ __forceinline__ void warp_rz_update(const double2 *Am, const double2 *Uo, double2 *U,
+                                               int lane) {
+  if (lane < 4) {
+    const double2 a = Am[3];
+    const double r = hypot(a.x, a.y);
+    double2 v = make_double2(lane == 0 ? 1.0 : 0.0, 0.0);
+    if (lane == 3) v = r > 0.0 ? make_double2(a.x / r, a.y / r) : Uo[3];
+    U[lane] = v;
+  }
+  __syncwarp();
+}
+
 // Polar factor dispatcher: closed form for 2 x 2; for 4 x 4 and 8 x 8 the
 // Newton-Schulz iteration with a Jacobi finish when it does not converge
 // (near-singular A), or Jacobi alone when `jacobi` is set or a warm start v0
@@ -743,7 +760,10 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
     }
     __syncwarp();
     double2 *vs = (A.vstore && D > 2) ? A.vstore + (long long)s * A.vstride + A.voff : nullptr;
-    warp_polar<D>(Am, Vm, Pm, lane, vs, A.polar_jacobi != 0);
+    if (D == 2 && A.rz)
+      warp_rz_update(Am, Uo, Pm, lane);
+    else
+      warp_polar<D>(Am, Vm, Pm, lane, vs, A.polar_jacobi != 0);
     if (vs)
       for (int e = lane; e < DD; e += 32) vs[e] = Vm[e];
     double2 *sc = A.scratch + (long long)s * kScratch;

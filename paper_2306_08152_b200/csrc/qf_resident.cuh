@@ -23,7 +23,8 @@ __device__ unsigned long long qf_t_gather, qf_t_form, qf_t_polar, qf_n_upd;
 #endif
 
 struct GateDesc {
-  int m, d, kind, goff;   // goff: complex offset in the packed gates (VAR) or in cmats (CONST)
+  int m, d, kind, goff;   // kind 0 VARIABLE, 1 CONSTANT, 2 RZ; goff: complex offset in the
+                          // packed gates (VARIABLE, RZ) or in cmats (CONSTANT)
   int mask;               // basis bits of the location
   int voff;               // complex offset of the backward warm-start slot in vstore
   int abits[8];
@@ -283,7 +284,10 @@ __device__ void res_update(const ResidentArgs &A, const GateDesc &g, double2 *u,
 #ifdef QF_POLAR_COUNT
   const long long q2 = clock64();
 #endif
-  warp_polar<D>(Am, Vm, Pm, lane, vs ? Vm : nullptr, A.polar_jacobi != 0);  // u_new -> Pm
+  if (D == 2 && g.kind == 2)
+    warp_rz_update(Am, Uo, Pm, lane);  // R_z gate: analytic update
+  else
+    warp_polar<D>(Am, Vm, Pm, lane, vs ? Vm : nullptr, A.polar_jacobi != 0);  // u_new -> Pm
 #ifdef QF_POLAR_COUNT
   if (lane == 0) {
     const long long q3 = clock64();
@@ -307,7 +311,7 @@ __device__ void res_prepare_d(const ResidentArgs &A, const ResView &V, const dou
                               const GateDesc &g, int s, int forward, double2 *Lb, double2 *Rb,
                               double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm, int lane) {
   constexpr int DD = D * D;
-  if (g.kind == 0) {
+  if (g.kind != 1) {  // VARIABLE or RZ
     double2 *u = V.u0 + g.goff;
     double2 *vs = (A.vstore && D > 2)
                       ? A.vstore + (long long)s * A.vstride + g.voff + (forward ? DD : 0)
@@ -382,7 +386,7 @@ __device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
   __syncthreads();
   for (int k = 0; k < V.p; k++) {
     const GateDesc &g = gdesc[k];
-    const double2 *src = g.kind == 0 ? V.u0 + g.goff : V.cmats + g.goff;
+    const double2 *src = g.kind != 1 ? V.u0 + g.goff : V.cmats + g.goff;
     if (g.d == 2) {
       res_apply_left<2>(ct, g, V, src, Ls);
     } else if constexpr (MAXD >= 4) {
@@ -396,7 +400,7 @@ __device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
   if (A.vstore) {  // warm starts restart from I with every (re)build
     for (int k = 0; k < V.p; k++) {
       const GateDesc &g = gdesc[k];
-      if (g.kind != 0) continue;
+      if (g.kind == 1) continue;
       double2 *v = A.vstore + (long long)s * A.vstride + g.voff;
       for (int e = threadIdx.x; e < 2 * g.d * g.d; e += blockDim.x) {
         const int q = e % (g.d * g.d);
@@ -486,7 +490,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
       int fw2;
       const GateDesc &g2 = gdesc[gate_of(j2, fw2)];
       const int off = (j2 & 1) * 64;
-      if (g2.kind == 0) {
+      if (g2.kind != 1) {
 #ifdef QF_POLAR_COUNT
         const long long tg0 = clock64();
 #endif
@@ -518,7 +522,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
           if (has_next && serial) {  // prefetch u_old of the next gate (L2 latency
             int fw2;                 // hidden behind this sandwich)
             const GateDesc &g2 = gdesc[gate_of(j + 1, fw2)];
-            if (g2.kind == 0) {
+            if (g2.kind != 1) {
               const double2 *u2 = V.u0 + g2.goff;
 #pragma unroll
               for (int q = 0; q < 2; q++) {

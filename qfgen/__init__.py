@@ -25,6 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 VARIABLE, CONSTANT = 0, 1
+RZ = 2  # NEXT-4: parameterised R_z(theta) = diag(1, e^{i theta}), a VARIABLE-like gate
 
 PURPOSE_INIT = 1  # initial unitaries of the multistarts
 PURPOSE_TARGET = 2  # Haar targets
@@ -113,7 +114,7 @@ class Workload:
 
     @property
     def var_doubles(self):
-        return sum(2 * 4 ** len(l) for l, k in zip(self.locs, self.kinds) if k == VARIABLE)
+        return sum(2 * 4 ** len(l) for l, k in zip(self.locs, self.kinds) if k != CONSTANT)
 
     @property
     def target_seed(self):
@@ -139,19 +140,30 @@ class Workload:
 
 
 def initial_gates(n, locs, kinds, seed, start_begin, count, purpose=PURPOSE_INIT):
-    """Pack Haar gates for VARIABLE gates, gate order, row-major, interleaved."""
-    var_idx = [k for k, kd in enumerate(kinds) if kd == VARIABLE]
+    """Pack the starting values of the parameterised gates, gate order,
+    row-major, interleaved: Haar for VARIABLE gates; R_z(theta) with theta
+    uniform in [0, 2 pi) for RZ gates."""
+    var_idx = [k for k, kd in enumerate(kinds) if kd != CONSTANT]
     sizes = [2 * 4 ** len(locs[k]) for k in var_idx]
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     out = np.zeros((count, int(offs[-1])), dtype=np.float64)
     starts = np.arange(start_begin, start_begin + count, dtype=np.uint64)
-    for d in sorted({1 << len(locs[k]) for k in var_idx}):
-        ks = [j for j, k in enumerate(var_idx) if (1 << len(locs[k])) == d]
+    for d in sorted({1 << len(locs[k]) for k in var_idx if kinds[k] == VARIABLE}):
+        ks = [j for j, k in enumerate(var_idx) if (1 << len(locs[k])) == d and kinds[k] == VARIABLE]
         gate_ids = np.array([var_idx[j] for j in ks], dtype=np.uint64)
         keys = stream_key(seed, purpose, starts[:, None], gate_ids[None, :])
         us = haar(keys.ravel(), d).reshape(count, len(ks), d * d)
         for col, j in enumerate(ks):
             out[:, offs[j]:offs[j + 1]] = np.ascontiguousarray(us[:, col]).view(np.float64)
+    for j, k in enumerate(var_idx):
+        if kinds[k] != RZ:
+            continue
+        keys = stream_key(seed, purpose, starts, np.uint64(k))
+        th = 2 * np.pi * uniforms(keys, 1)[:, 0]
+        m = np.zeros((count, 4), dtype=np.complex128)
+        m[:, 0] = 1.0
+        m[:, 3] = np.exp(1j * th)
+        out[:, offs[j]:offs[j + 1]] = m.view(np.float64)
     return out
 
 
@@ -159,7 +171,7 @@ def unpack_gates(locs, kinds, packed):
     """Inverse of the packing: list of (d, d) complex (None for CONSTANT)."""
     out, off = [], 0
     for l, k in zip(locs, kinds):
-        if k != VARIABLE:
+        if k == CONSTANT:
             out.append(None)
             continue
         d = 1 << len(l)
@@ -176,7 +188,7 @@ def circuit_unitary(n, locs, kinds, const_mats, packed):
     T = np.eye(N, dtype=np.complex128).reshape((2,) * (2 * n))
     gates = unpack_gates(locs, kinds, packed)
     for l, k, u, c in zip(locs, kinds, gates, const_mats):
-        g = u if k == VARIABLE else np.asarray(c, dtype=np.complex128)
+        g = u if k != CONSTANT else np.asarray(c, dtype=np.complex128)
         m = len(l)
         G = g.reshape((2,) * (2 * m))
         # contract gate input legs with the output legs l of T
