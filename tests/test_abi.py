@@ -19,7 +19,7 @@ GOLD = os.path.join(ROOT, "tests", "golden")
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "qf.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(qf_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(qf_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol():
