@@ -430,6 +430,7 @@ struct Engine {
     const auto rt = row_tiles(c.n, A.b.m);
     A.RT = rt.first;
     A.tiles_per_start = rt.second;
+    A.dmma = rows_dmma;
     const size_t tile_bytes = (size_t)A.RT * D * N * 16;
     A.stages = (int)std::max<size_t>(2, std::min<size_t>(4, (96 * 1024) / tile_bytes));
     const size_t smem = A.stages * tile_bytes + 2 * D * D * 16 + 2 * A.stages * 8 + 2 * kMaxTileRows * 4 + 16 * 4;
@@ -521,6 +522,7 @@ struct Engine {
     }
   }
   int reg_variant = getenv("QF_REG") ? atoi(getenv("QF_REG")) : 2;
+  int rows_dmma = getenv("QF_ROWS_DMMA") ? atoi(getenv("QF_ROWS_DMMA")) : 1;
   int reg_grid[4] = {0, 0, 0, 0};
 
   cudaError_t sandwich(const SandwichArgs &A) {

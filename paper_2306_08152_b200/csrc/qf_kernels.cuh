@@ -960,6 +960,7 @@ struct RowTileArgs {
   int rdag;
   int RT;               // row-rests per tile
   int tiles_per_start;  // (N/d)/RT
+  int dmma;             // d = 8: left multiply on the FP64 tensor path (mma.m8n8k4)
   int stages;           // ring depth
   // phase-2 bank spreading: item c runs over the gate's local column index
   // in the order b ^ rot[c & 7] (a permutation of 0..d-1), so that the 8
@@ -1104,7 +1105,43 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
     ptx::mbar_wait(&full[st], (uint32_t)((j / A.stages) & 1));
     double2 *tile = tiles + (size_t)st * tile_elems;
     // phase 1: left multiply, one column of one row group per item
-    for (int it = tid; it < A.RT * N; it += kRowThreads) {
+    if constexpr (D == 8) {
+      if (A.dmma) {
+        // on the FP64 tensor path: Y = L X per 8-column chunk of a row group
+        // as 8 x mma.m8n8k4.f64 (complex = 4 real products per k-block);
+        // L stays in registers, X and Y move as one 16-byte access per lane
+        // per k-block / output pair -- a quarter of the shared-memory
+        // wavefronts of the FMA form (which is bound by them at d = 8)
+        const int lane = tid & 31, warp = tid >> 5;
+        const int fr = lane >> 2, fk = lane & 3;
+        double lr[2], li[2], nli[2];
+#pragma unroll
+        for (int kb = 0; kb < 2; kb++) {
+          const double2 l = Ls[fr * 8 + kb * 4 + fk];  // A[m = fr][k = kb*4 + fk]
+          lr[kb] = l.x;
+          li[kb] = l.y;
+          nli[kb] = -l.y;
+        }
+        const int chunks = A.RT * (N >> 3);
+        for (int ch = warp; ch < chunks; ch += kRowThreads / 32) {
+          const int rl = ch / (N >> 3), col0 = (ch - rl * (N >> 3)) << 3;
+          double2 *base = tile + (size_t)rl * 8 * N + col0;
+          double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+#pragma unroll
+          for (int kb = 0; kb < 2; kb++) {
+            const double2 x = base[(kb * 4 + fk) * N + fr];  // B[k = kb*4 + fk][n = fr]
+            ptx::dmma(cr0, cr1, lr[kb], x.x);
+            ptx::dmma(cr0, cr1, nli[kb], x.y);
+            ptx::dmma(ci0, ci1, lr[kb], x.y);
+            ptx::dmma(ci0, ci1, li[kb], x.x);
+          }
+          __syncwarp();  // every lane has read its X before Y overwrites it
+          base[fr * N + 2 * fk] = make_double2(cr0, ci0);  // C[m = fr][n = 2 fk + {0, 1}]
+          base[fr * N + 2 * fk + 1] = make_double2(cr1, ci1);
+        }
+      }
+    }
+    for (int it = tid; it < (D == 8 && A.dmma ? 0 : A.RT * N); it += kRowThreads) {
       const int rl = it / N, col = it - rl * N;
       double2 *base = tile + (size_t)rl * D * N + col;
       double2 x[D];
@@ -1120,9 +1157,46 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
     }
     if (has_r) {
       csync();
+      if constexpr (D == 8) {
+        if (A.dmma) {
+          // phase 2 on the tensor path: 8 items (rows of the mma) x 8 local
+          // columns; R in registers (B[k][n] = R[k][n]); each lane gathers
+          // its item's columns ins(k, c) and writes the item's outputs
+          const int lane = tid & 31, warp = tid >> 5;
+          const int fr = lane >> 2, fk = lane & 3;
+          double rr[2], ri[2], nri[2];
+#pragma unroll
+          for (int kb = 0; kb < 2; kb++) {
+            const double2 r = Rs[(kb * 4 + fk) * 8 + fr];
+            rr[kb] = r.x;
+            ri[kb] = r.y;
+            nri[kb] = -r.y;
+          }
+          const int groups = (A.RT * N) >> 3;
+          for (int gi = warp; gi < groups; gi += kRowThreads / 32) {
+            const int it = (gi << 3) + fr;
+            const int rl = it / N, rem = it - rl * N;
+            const int a = rem / NC, c = rem - a * NC;
+            double2 *row = tile + (size_t)(rl * D + a) * N;
+            const int cb = spread_rest(A.b, c);
+            double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+#pragma unroll
+            for (int kb = 0; kb < 2; kb++) {
+              const double2 y = row[cb | sab[kb * 4 + fk]];  // A[m = fr][k = kb*4 + fk]
+              ptx::dmma(cr0, cr1, y.x, rr[kb]);
+              ptx::dmma(cr0, cr1, y.y, nri[kb]);
+              ptx::dmma(ci0, ci1, y.x, ri[kb]);
+              ptx::dmma(ci0, ci1, y.y, rr[kb]);
+            }
+            __syncwarp();
+            row[cb | sab[2 * fk]] = make_double2(cr0, ci0);  // C[m = fr][n = 2 fk + {0, 1}]
+            row[cb | sab[2 * fk + 1]] = make_double2(cr1, ci1);
+          }
+        }
+      }
       // phase 2: right multiply, d columns ins(b, c) of one row per item,
       // local column order permuted by m = rot[c & 7] (R's indices follow)
-      for (int it = tid; it < A.RT * N; it += kRowThreads) {
+      for (int it = tid; it < (D == 8 && A.dmma ? 0 : A.RT * N); it += kRowThreads) {
         const int rl = it / N, rem = it - rl * N;
         const int a = rem / NC, c = rem - a * NC;
         double2 *row = tile + (size_t)(rl * D + a) * N;
