@@ -245,8 +245,18 @@ def _c5():
     return locs, [VARIABLE] * 200, [None] * 200
 
 
+def _round(n, p):
+    """C5's pattern on n qubits: a cyclic round of n-1 U(4) on (i, i+1), then
+    n-2 U(8) on (i, i+1, i+2), truncated to p gates."""
+    locs = []
+    while len(locs) < p:
+        locs += [(i, i + 1) for i in range(n - 1)] + [(i, i + 1, i + 2) for i in range(n - 2)]
+    return locs[:p], [VARIABLE] * p, [None] * p
+
+
 def workload(name: str) -> Workload:
-    """The configs of BASELINE.json / SURVEY.md Sec. 8d."""
+    """The configs of BASELINE.json / SURVEY.md Sec. 8d (C1-C5, C2+, C3+) and
+    the NEXT-3 size probes C6 (n = 10) and C7 (n = 12)."""
     if name == "C1":
         l, k, c = _c1()
         return Workload("C1", 2, l, k, c, 4, 10000, "haar", 1,
@@ -275,6 +285,14 @@ def workload(name: str) -> Workload:
         l, k, c = _ladder(4, 40)
         return Workload("C3+", 4, l, k, c, 1024, 2000, "haar", 7,
                         "4-qubit ladder of 40 VAR U(4) vs Haar, 1024 starts")
+    if name == "C6":
+        l, k, c = _round(10, 60)
+        return Workload("C6", 10, l, k, c, 256, 1000, "self", 8,
+                        "10-qubit round of VAR U(4) + U(8) (C5 pattern), 60 gates, self-target, 256 starts")
+    if name == "C7":
+        l, k, c = _round(12, 40)
+        return Workload("C7", 12, l, k, c, 32, 1000, "self", 9,
+                        "12-qubit round of VAR U(4) + U(8) (C5 pattern), 40 gates, self-target, 32 starts")
     raise KeyError(name)
 
 

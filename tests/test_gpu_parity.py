@@ -139,6 +139,25 @@ def test_parity_n10_tile_kernel():
     _compare(gpu, orc, idx, 2, 2 ** n)
 
 
+@pytest.mark.parametrize("n,S", [(11, 2), (12, 1)])
+def test_parity_next3_sizes(n, S):
+    """NEXT-3 range (n = 9-12, ct 4-256 MiB per start): one sweep of a
+    3-gate template (arities 1-3) on the streaming engine; target = a
+    Kronecker product of Haar blocks (a dense Haar 4096 x 4096 is not needed
+    to exercise every index path)."""
+    locs, kinds, cm = qfgen.random_template(n, 3, arities=(1, 2, 3), seed=50 + n)
+    rng = np.random.default_rng(n)
+    V = np.array([[1.0]])
+    for b in (3, 3, 3, n - 9):
+        if b:
+            q, r = np.linalg.qr(rng.standard_normal((2 ** b, 2 ** b)) +
+                                1j * rng.standard_normal((2 ** b, 2 ** b)))
+            V = np.kron(V, q * (np.diag(r) / abs(np.diag(r))))
+    init = qfgen.initial_gates(n, locs, kinds, 3100 + n, 0, S)
+    gpu, orc, idx = _run_pair(n, locs, kinds, cm, V, init, R=1, max_iters=1)
+    _compare(gpu, orc, idx, 1, 2 ** n)
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("name", ["C1", "C2+"])
 def test_parity_full_run(name, engine):
