@@ -432,7 +432,7 @@ struct Engine {
     A.tiles_per_start = rt.second;
     A.dmma = rows_dmma;
     const size_t tile_bytes = (size_t)A.RT * D * N * 16;
-    A.stages = (int)std::max<size_t>(2, std::min<size_t>(4, (96 * 1024) / tile_bytes));
+    A.stages = (int)std::max<size_t>(2, std::min<size_t>(4, (rows_smem_kb * 1024) / tile_bytes));
     const size_t smem = A.stages * tile_bytes + 2 * D * D * 16 + 2 * A.stages * 8 + 2 * kMaxTileRows * 4 + 16 * 4;
     {
       // bank spreading of phase 2: the gate's bits among basis positions
@@ -468,19 +468,19 @@ struct Engine {
       A.tpart_stride = L.max_parts;
       tpart_tiles = A.tiles_per_start;
     }
+    auto kern = rows_minb >= 3 ? k_sandwich_rows<D, 3> : rows_minb == 2 ? k_sandwich_rows<D, 2>
+                                                                       : k_sandwich_rows<D, 1>;
     int &grid = rows_grid[ilog2(D)][A.stages];
     if (grid == 0) {
-      cudaFuncSetAttribute(k_sandwich_rows<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sandwich_rows<D>, kRowThreads + 32,
-                                                    smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRowThreads + 32, smem);
       grid = std::max(1, per_sm) * nsm;
     }
     const long long total = (long long)S * A.tiles_per_start;
     const int g = (int)std::max<long long>(1, std::min<long long>(grid, total));
     const int slot = prof.on ? prof.open(0, st) : -1;
-    k_sandwich_rows<D><<<g, kRowThreads + 32, smem, st>>>(A);
+    kern<<<g, kRowThreads + 32, smem, st>>>(A);
     if (slot >= 0) prof.close(slot, st);
     launches++;
     sw_ctx[ctx]++;
@@ -523,6 +523,8 @@ struct Engine {
   }
   int reg_variant = getenv("QF_REG") ? atoi(getenv("QF_REG")) : 2;
   int rows_dmma = getenv("QF_ROWS_DMMA") ? atoi(getenv("QF_ROWS_DMMA")) : 1;
+  int rows_smem_kb = getenv("QF_ROWS_SMEM_KB") ? atoi(getenv("QF_ROWS_SMEM_KB")) : 96;
+  int rows_minb = getenv("QF_ROWS_MINB") ? atoi(getenv("QF_ROWS_MINB")) : 2;
   int reg_grid[4] = {0, 0, 0, 0};
 
   cudaError_t sandwich(const SandwichArgs &A) {
@@ -1377,5 +1379,14 @@ extern "C" void qf_debug_polar_counts(unsigned long long *out) {
   cudaMemcpyFromSymbol(&out[7], qf::qf_t_form, 8);
   cudaMemcpyFromSymbol(&out[8], qf::qf_t_polar, 8);
   cudaMemcpyFromSymbol(&out[9], qf::qf_n_upd, 8);
+}
+// row-tile d = 8 phase timers: wait-for-data, phase 1, phase 2, epilogue, tiles
+extern "C" void qf_debug_rows_counts(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&out[0], qf::qf_rt_wait, 8);
+  cudaMemcpyFromSymbol(&out[1], qf::qf_rt_p1, 8);
+  cudaMemcpyFromSymbol(&out[2], qf::qf_rt_p2, 8);
+  cudaMemcpyFromSymbol(&out[3], qf::qf_rt_epi, 8);
+  cudaMemcpyFromSymbol(&out[4], qf::qf_rt_tiles, 8);
 }
 #endif

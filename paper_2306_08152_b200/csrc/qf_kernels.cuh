@@ -27,6 +27,10 @@ constexpr int kMaxQubits = 12;
 #ifdef QF_POLAR_COUNT
 __device__ unsigned long long qf_polar_sweeps;  // microbenchmark instrumentation only
 __device__ unsigned long long qf_ns_iters, qf_ns_calls;
+#ifdef QF_POLAR_COUNT
+// row-tile kernel phase timers (consumer thread 0; debug build only)
+__device__ unsigned long long qf_rt_wait, qf_rt_p1, qf_rt_p2, qf_rt_epi, qf_rt_tiles;
+#endif
 #endif
 constexpr int kTileItems = 256;   // work items per sandwich tile (= threads)
 constexpr int kScratch = 64;      // complex per start in the u_old scratch
@@ -990,8 +994,8 @@ constexpr int kMaxTileRows = 64;
 // back (its own bulk group) and reuses the slot for the tile `stages` ahead.
 //   full[st]     : TMA bytes of the tile in stage st have landed
 //   computed[st] : the consumers are done with the tile in stage st
-template <int D>
-__global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTileArgs A) {
+template <int D, int MINB = 2>
+__global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const RowTileArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int N = A.N;
   const int rows = A.RT * D;
@@ -1102,7 +1106,13 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
     }
     int *rid = rid_buf + (j & 1) * kMaxTileRows;  // global row of each tile row
     if (tid < rows) rid[tid] = spread_rest(A.b, tt * A.RT + tid / D) | A.b.abits[tid % D];
+#ifdef QF_POLAR_COUNT
+    const long long tq0 = clock64();
+#endif
     ptx::mbar_wait(&full[st], (uint32_t)((j / A.stages) & 1));
+#ifdef QF_POLAR_COUNT
+    const long long tq1 = clock64();
+#endif
     double2 *tile = tiles + (size_t)st * tile_elems;
     // phase 1: left multiply, one column of one row group per item
     if constexpr (D == 8) {
@@ -1155,6 +1165,9 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
         base[a * N] = acc;
       }
     }
+#ifdef QF_POLAR_COUNT
+    const long long tq2 = clock64();
+#endif
     if (has_r) {
       csync();
       if constexpr (D == 8) {
@@ -1216,6 +1229,9 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
       }
     }
     csync();
+#ifdef QF_POLAR_COUNT
+    const long long tq3 = clock64();
+#endif
     // fused epilogue: partial environment / trace of the next step (fixed
     // order over the tile's rows => independent of batch and sharding)
     if (A.nx_env) {
@@ -1247,6 +1263,16 @@ __global__ void __launch_bounds__(kRowThreads + 32) k_sandwich_rows(const RowTil
     ptx::fence_proxy_async_smem();
     csync();
     if (tid == 0) ptx::mbar_arrive(&computed[st]);
+#ifdef QF_POLAR_COUNT
+    if (tid == 0 && D == 8) {
+      const long long tq4 = clock64();
+      atomicAdd(&qf_rt_wait, (unsigned long long)(tq1 - tq0));
+      atomicAdd(&qf_rt_p1, (unsigned long long)(tq2 - tq1));
+      atomicAdd(&qf_rt_p2, (unsigned long long)(tq3 - tq2));
+      atomicAdd(&qf_rt_epi, (unsigned long long)(tq4 - tq3));
+      atomicAdd(&qf_rt_tiles, 1ull);
+    }
+#endif
   }
 }
 

@@ -36,3 +36,10 @@ if out[5]:
 if out[9]:
     print(f"  gather (all threads, before the barrier) {out[6] / out[9]:.0f}, form A {out[7] / out[9]:.0f}, "
           f"polar {out[8] / out[9]:.0f} cycles")
+
+rc = (ctypes.c_ulonglong * 5)()
+qf.lib().qf_debug_rows_counts(rc)
+if rc[4]:
+    print(f"  row-tile d=8 per tile (consumer thread 0): wait {rc[0] / rc[4]:.0f}, phase 1 "
+          f"{rc[1] / rc[4]:.0f}, phase 2 {rc[2] / rc[4]:.0f}, epilogue+handoff {rc[3] / rc[4]:.0f} cycles "
+          f"({rc[4]} tiles)")
