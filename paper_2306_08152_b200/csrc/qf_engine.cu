@@ -220,7 +220,7 @@ std::pair<int, int> row_tiles(int n, int m) {
 struct Layout {
   size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
       rec_slot, rec_starts, rec_cost, rec_gates, summary, best, part, tpart, vstore, vslots,
-      gdesc, plat, total;
+      gdesc, plat, gops, total;
   long long vstride;  // complex per start in vstore (sum over VARIABLE gates of 2 d^2)
   int nvslots;
   int ring;
@@ -272,6 +272,7 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
   L.vslots = take((size_t)std::max(1, L.nvslots) * 8);
   L.gdesc = take((size_t)std::max(1, c.p) * sizeof(GateDesc));
   L.plat = take(S * 4);
+  L.gops = take(S * 128 * 16);  // grouped steps: Lp, Rp (<= 8 x 8) per start
   L.total = o;
   return L;
 }
@@ -282,30 +283,33 @@ int ilog2(int x) {
   return k;
 }
 
-Bits make_bits(const qf_circuit_s &c, int k) {
+Bits make_bits_loc(int n, const int *loc, int m) {
   Bits b{};
-  b.n = c.n;
-  b.m = c.arity[k];
-  b.d = 1 << b.m;
-  const int *loc = &c.loc[c.loc_off[k]];
+  b.n = n;
+  b.m = m;
+  b.d = 1 << m;
   for (int a = 0; a < b.d; a++) {
     int x = 0;
-    for (int t = 0; t < b.m; t++) x |= ((a >> (b.m - 1 - t)) & 1) << (c.n - 1 - loc[t]);
+    for (int t = 0; t < m; t++) x |= ((a >> (m - 1 - t)) & 1) << (n - 1 - loc[t]);
     b.abits[a] = x;
   }
   int r = 0;
-  for (int pos = 0; pos < c.n; pos++) {
+  for (int pos = 0; pos < n; pos++) {
     bool in = false;
-    for (int t = 0; t < b.m; t++) in |= (c.n - 1 - loc[t]) == pos;
+    for (int t = 0; t < m; t++) in |= (n - 1 - loc[t]) == pos;
     if (!in) b.rest_pos[r++] = pos;
   }
   return b;
 }
 
+Bits make_bits(const qf_circuit_s &c, int k) {
+  return make_bits_loc(c.n, &c.loc[c.loc_off[k]], c.arity[k]);
+}
+
 // tile geometry of k_sandwich for gate k (see SandwichArgs)
-void make_tiles(const qf_circuit_s &c, int k, SandwichArgs &A) {
-  A.b = make_bits(c, k);
-  const int N = 1 << c.n, d = A.b.d, m = A.b.m;
+void make_tiles_loc(int n, const int *loc, int m, SandwichArgs &A) {
+  A.b = make_bits_loc(n, loc, m);
+  const int N = 1 << n, d = A.b.d;
   A.N = N;
   A.DC = std::min(N, kTileItems);
   A.CT = A.DC / d;
@@ -315,8 +319,7 @@ void make_tiles(const qf_circuit_s &c, int k, SandwichArgs &A) {
   A.log_ct = ilog2(A.CT);
   A.log_dc = ilog2(A.DC);
   std::vector<int> free_bits;
-  const int *loc = &c.loc[c.loc_off[k]];
-  for (int t = 0; t < m; t++) free_bits.push_back(c.n - 1 - loc[t]);
+  for (int t = 0; t < m; t++) free_bits.push_back(n - 1 - loc[t]);
   for (int q = 0; q < A.log_ct; q++) free_bits.push_back(A.b.rest_pos[q]);
   std::sort(free_bits.begin(), free_bits.end());
   for (int q = 0; q < A.log_dc; q++) A.col_dep[q] = free_bits[q];
@@ -325,11 +328,56 @@ void make_tiles(const qf_circuit_s &c, int k, SandwichArgs &A) {
   };
   for (int b = 0; b < d; b++) {
     int x = 0;
-    for (int t = 0; t < m; t++)
-      x |= ((b >> (m - 1 - t)) & 1) << index_of(c.n - 1 - loc[t]);
+    for (int t = 0; t < m; t++) x |= ((b >> (m - 1 - t)) & 1) << index_of(n - 1 - loc[t]);
     A.jt_b[b] = x;
   }
   for (int q = 0; q < A.log_ct; q++) A.jt_rest[q] = index_of(A.b.rest_pos[q]);
+}
+
+void make_tiles(const qf_circuit_s &c, int k, SandwichArgs &A) {
+  make_tiles_loc(c.n, &c.loc[c.loc_off[k]], c.arity[k], A);
+}
+
+// NEXT-3 grouping of the sweep schedule (2p steps: backward p-1..0, forward
+// 0..p-1) into runs whose locations fit in <= umax qubits (a wider gate is a
+// group of its own); groups never span sweeps.
+struct StepGroup {
+  std::vector<int> wq;                   // qubits of W, ascending
+  std::vector<std::pair<int, int>> steps;  // (gate, forward)
+};
+
+// NEXT-3 grouped steps on the streaming engine, groups of <= umax qubits:
+// default 2 (a group then flushes with the HBM-bound d <= 4 kernels; measured
+// 2.0x on the U3 + CNOT template C8, neutral on ladders); QF_GROUP=3 also
+// forms 3-qubit groups (d = 8 flush, FP64-bound: +15 % on C5, 0 on C6),
+// QF_GROUP=0 runs one pass per step
+int group_default() {
+  const char *e = getenv("QF_GROUP");
+  return e ? std::max(0, std::min(3, atoi(e))) : 2;
+}
+
+std::vector<StepGroup> make_groups(const qf_circuit_s &c, int umax) {
+  std::vector<StepGroup> out;
+  StepGroup cur;
+  for (int j = 0; j < 2 * c.p; j++) {
+    const int fw = j >= c.p, k = fw ? j - c.p : c.p - 1 - j;
+    std::vector<int> u = cur.wq;
+    for (int t = 0; t < c.arity[k]; t++) u.push_back(c.loc[c.loc_off[k] + t]);
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    const int lim = std::min(3, std::max(umax, c.arity[k]));
+    if (!cur.steps.empty() && ((int)u.size() > lim || (int)cur.steps.size() >= kGroupMax)) {
+      out.push_back(cur);
+      cur = StepGroup{};
+      u.clear();
+      for (int t = 0; t < c.arity[k]; t++) u.push_back(c.loc[c.loc_off[k] + t]);
+      std::sort(u.begin(), u.end());
+    }
+    cur.wq = u;
+    cur.steps.push_back({k, fw});
+  }
+  if (!cur.steps.empty()) out.push_back(cur);
+  return out;
 }
 
 struct Engine {
@@ -656,6 +704,71 @@ struct Engine {
     return sandwich(A);
   }
 
+  // NEXT-3: one group of steps (see k_group): T gather + every update in one
+  // warp-per-start launch, then one sandwich pass with the accumulated (Lp, Rp)
+  cudaError_t group_steps(const StepGroup &G) {
+    const int w = (int)G.wq.size();
+    GroupArgs A{};
+    A.bw = make_bits_loc(c.n, G.wq.data(), w);
+    A.N = N;
+    A.ct = ct();
+    A.ct_stride = (long long)N * N;
+    A.active = active();
+    A.n_active = n_active();
+    A.gates = reinterpret_cast<double2 *>(gates());
+    A.gstride = c.var_doubles / 2;
+    A.cmats = cmats();
+    A.beta = p.beta;
+    A.polar_jacobi = polar_jacobi ? 1 : 0;
+    A.ops = reinterpret_cast<double2 *>(ws + L.gops);
+    A.ops_stride = 128;
+    A.nsteps = (int)G.steps.size();
+    for (int i = 0; i < A.nsteps; i++) {
+      const int k = G.steps[i].first, m = c.arity[k];
+      GroupStep &g = A.st[i];
+      g.kind = c.kind[k] == QF_GATE_CONSTANT ? 1 : (c.kind[k] == QF_GATE_RZ ? 2 : 0);
+      g.forward = G.steps[i].second;
+      g.d = 1 << m;
+      g.goff = g.kind != 1 ? c.var_off[k] / 2 : c.const_off[k] / 2;
+      for (int a = 0; a < g.d; a++) {
+        int x = 0;
+        for (int t = 0; t < m; t++) {
+          const int q = c.loc[c.loc_off[k] + t];
+          const int iw = (int)(std::find(G.wq.begin(), G.wq.end(), q) - G.wq.begin());
+          x |= ((a >> (m - 1 - t)) & 1) << (w - 1 - iw);
+        }
+        g.gab[a] = x;
+      }
+      g.gmask = g.gab[g.d - 1];
+    }
+    const int grid = std::max(1, std::min((S + kEnvWarps - 1) / kEnvWarps, nsm * 16));
+    const int slot = prof.on ? prof.open(1, st) : -1;
+    if (w == 1) k_group<2><<<grid, 32 * kEnvWarps, 0, st>>>(A);
+    else if (w == 2) k_group<4><<<grid, 32 * kEnvWarps, 0, st>>>(A);
+    else k_group<8><<<grid, 32 * kEnvWarps, 0, st>>>(A);
+    if (slot >= 0) prof.close(slot, st);
+    launches++;
+    env_ctx[ctx]++;
+    env_bytes_ctx[ctx] += (long long)16 * N * (1 << w) + 64LL * 16 * A.nsteps;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    SandwichArgs B{};
+    make_tiles_loc(c.n, G.wq.data(), w, B);
+    B.ct = ct();
+    B.ct_stride = (long long)N * N;
+    B.active = active();
+    B.n_active = n_active();
+    B.lsrc = reinterpret_cast<const double2 *>(ws + L.gops);
+    B.lstride = 128;
+    B.ldag = 0;
+    B.rsrc = B.lsrc + 64;
+    B.rstride = 128;
+    B.rdag = 0;
+    next_k = -1;
+    next_trace = false;
+    return sandwich(B);
+  }
+
   // InitCircuitTensor for the active starts
   cudaError_t init_ct() {
     const long long NN = (long long)N * N;
@@ -972,10 +1085,16 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       if (p.reset_iters > 0 && it % p.reset_iters == 0) QF_CHECK(E.init_ct());
     }
   } else {
+    const int umax = group_default();
+    const std::vector<StepGroup> groups = umax > 0 ? make_groups(c, umax) : std::vector<StepGroup>{};
     for (int it = 1; it <= p.max_iters; it++) {
       E.ctx = it - 1;  // this sweep runs on the starts active after sweep it-1
-      for (int k = c.p - 1; k >= 0; k--) QF_CHECK(E.step(k, 0));
-      for (int k = 0; k < c.p; k++) QF_CHECK(E.step(k, 1));
+      if (!groups.empty()) {
+        for (const auto &G : groups) QF_CHECK(E.group_steps(G));
+      } else {
+        for (int k = c.p - 1; k >= 0; k--) QF_CHECK(E.step(k, 0));
+        for (int k = 0; k < c.p; k++) QF_CHECK(E.step(k, 1));
+      }
       QF_CHECK(E.trace(it));
       E.ctx = it;
       if (p.reset_iters > 0 && it % p.reset_iters == 0 && it < p.max_iters) QF_CHECK(E.init_ct());

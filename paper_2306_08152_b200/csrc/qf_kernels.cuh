@@ -1361,6 +1361,215 @@ __global__ void __launch_bounds__(NT, MINB) k_sandwich_reg(const SandwichArgs A)
   }
 }
 
+// ------------------------------------------------------------------ grouped steps (NEXT-3)
+// A group is a run of consecutive gate steps of the sweep whose locations lie
+// in one small qubit set W (|W| <= 3).  Their updates need the circuit tensor
+// only through T = PT_{not W}(ct) (4^|W| complex per start): with the group's
+// earlier factors pending as Lp (rows) and Rp (columns) on W,
+//   PT_{not G}(E(Lp) ct E(Rp)) = PT_{W \ G}(Lp T Rp),
+// since partial traces over qubits outside W commute with operators on W.
+// k_group gathers T once, runs every step's update from it (warp per start),
+// accumulates Lp <- E_W(L_k) Lp, Rp <- Rp E_W(R_k), and one sandwich pass with
+// (Lp, Rp) on W then applies the whole group: one HBM pass per group instead
+// of one per step.  Same steps, same order; only the association differs.
+constexpr int kGroupMax = 48;
+
+struct GroupStep {
+  int kind;     // 0 VARIABLE, 1 CONSTANT, 2 RZ
+  int forward;  // sweep half
+  int d;        // gate dimension 2^m
+  int goff;     // complex offset: packed gates (kind != 1) or cmats (kind 1)
+  int gmask;    // W-local bits of the gate's qubits
+  int gab[8];   // W-local index of gate-local index a
+};
+
+struct GroupArgs {
+  Bits bw;  // W as a pseudo-gate (T gather, flush)
+  int N;
+  const double2 *ct;
+  long long ct_stride;
+  const int *active;
+  const int *n_active;
+  double2 *gates;
+  long long gstride;
+  const double2 *cmats;
+  double beta;
+  int polar_jacobi;
+  double2 *ops;  // per start: Lp [64], Rp [64]
+  long long ops_stride;
+  int nsteps;
+  GroupStep st[kGroupMax];
+};
+
+// C = A B for DW x DW complex in warp shared memory (lanes over outputs)
+template <int DW>
+__device__ __forceinline__ void group_mm(const double2 *Am, const double2 *Bm, double2 *Cm,
+                                         int lane) {
+  for (int o = lane; o < DW * DW; o += 32) {
+    const int r = o / DW, c = o % DW;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < DW; k++) acc = cfma(Am[r * DW + k], Bm[k * DW + c], acc);
+    Cm[o] = acc;
+  }
+  __syncwarp();
+}
+
+template <int DW>
+__global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant__ GroupArgs A) {
+  constexpr int DD = DW * DW;
+  __shared__ double2 smem[kEnvWarps][4 * DD + 4 * 64];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2 *T = smem[w];
+  double2 *Lp = T + DD;
+  double2 *Rp = Lp + DD;
+  double2 *M = Rp + DD;
+  double2 *Uo = M + DD;
+  double2 *Pm = Uo + 64;
+  double2 *Am = Pm + 64;
+  double2 *Vm = Am + 64;
+  const int nact = *A.n_active;
+  const int R = 1 << (A.bw.n - A.bw.m);
+  const int N = A.N;
+  constexpr int SPLIT = DD >= 32 ? 1 : 32 / DD;
+  constexpr int OPL = DD >= 32 ? DD / 32 : 1;
+  for (int ai = blockIdx.x * kEnvWarps + w; ai < nact; ai += gridDim.x * kEnvWarps) {
+    const int s = A.active[ai];
+    // T = PT_{not W}(ct), rests ascending per lane, fixed xor tree
+    const double2 *cts = A.ct + (long long)s * A.ct_stride;
+    const int k = lane % SPLIT;
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {
+      const int o = (lane / SPLIT) + q * (32 / SPLIT);
+      const int a = o / DW, b = o % DW;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int r = k; r < R; r += SPLIT) {
+        const int sp = spread_rest(A.bw, r);
+        const double2 v = cts[(long long)(sp | A.bw.abits[a]) * N + (sp | A.bw.abits[b])];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+#pragma unroll
+      for (int off = 1; off < SPLIT; off <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+      }
+      if (k == 0) T[o] = acc;
+    }
+    for (int o = lane; o < DD; o += 32) {
+      const double2 one = make_double2(o / DW == o % DW ? 1.0 : 0.0, 0.0);
+      Lp[o] = one;
+      Rp[o] = one;
+    }
+    __syncwarp();
+    double2 *ug = A.gates + (long long)s * A.gstride;
+    for (int j = 0; j < A.nsteps; j++) {
+      const GroupStep &g = A.st[j];
+      const int d = g.d, dd = d * d;
+      // P = PT_{W \ G}(Lp T Rp)
+      group_mm<DW>(Lp, T, M, lane);
+      group_mm<DW>(M, Rp, Am, lane);  // Am: scratch DW x DW (<= 64)
+      const int nr = DW / d;
+      for (int o = lane; o < dd; o += 32) {
+        const int a = o / d, b = o % d;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int r = 0; r < nr; r++) {
+          const int xr = insert_zeros(r, g.gmask);
+          const double2 v = Am[(xr | g.gab[a]) * DW + (xr | g.gab[b])];
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        Pm[o] = acc;
+      }
+      __syncwarp();
+      // the step's factors L (rows) and R (columns) into Uo (L) / Vm (R)
+      if (g.kind != 1) {
+        double2 *u = ug + g.goff;
+        for (int e = lane; e < dd; e += 32) Uo[e] = u[e];
+        __syncwarp();
+        for (int o = lane; o < dd; o += 32) {  // A = E^dagger (as k_env_polar)
+          const int r = o / d, c = o % d;
+          double2 acc = make_double2(0.0, 0.0);
+          if (!g.forward) {
+            for (int kk = 0; kk < d; kk++) acc = cfma_cj(Pm[kk * d + r], Uo[kk * d + c], acc);
+          } else {
+            for (int kk = 0; kk < d; kk++) {
+              const double2 x = Uo[r * d + kk], pv = Pm[c * d + kk];
+              acc.x = fma(x.x, pv.x, acc.x);
+              acc.x = fma(x.y, pv.y, acc.x);
+              acc.y = fma(x.y, pv.x, acc.y);
+              acc.y = fma(-x.x, pv.y, acc.y);
+            }
+          }
+          if (A.beta != 0.0) {
+            acc = cscale(acc, 1.0 - A.beta);
+            acc.x = fma(A.beta, Uo[o].x, acc.x);
+            acc.y = fma(A.beta, Uo[o].y, acc.y);
+          }
+          Am[o] = acc;
+        }
+        __syncwarp();
+        if (d == 2) {
+          if (g.kind == 2) warp_rz_update(Am, Uo, Pm, lane);
+          else warp_polar<2>(Am, Vm, Pm, lane, nullptr, A.polar_jacobi != 0);
+        } else if (d == 4) {
+          warp_polar<4>(Am, Vm, Pm, lane, nullptr, A.polar_jacobi != 0);
+        } else {
+          warp_polar<8>(Am, Vm, Pm, lane, nullptr, A.polar_jacobi != 0);
+        }
+        for (int e = lane; e < dd; e += 32) u[e] = Pm[e];  // u_new
+        // backward: L = u_old^H, R = u_new;  forward: L = u_new, R = u_old^H
+        for (int e = lane; e < dd; e += 32) {
+          const int i = e / d, kk = e % d;
+          const double2 od = cconj(Uo[kk * d + i]), nw = Pm[e];
+          Am[e] = g.forward ? nw : od;
+          Vm[e] = g.forward ? od : nw;
+        }
+      } else {
+        const double2 *cm = A.cmats + g.goff;
+        for (int e = lane; e < dd; e += 32) {
+          const int i = e / d, kk = e % d;
+          const double2 cd = cconj(cm[kk * d + i]), cv = cm[e];
+          Am[e] = g.forward ? cv : cd;
+          Vm[e] = g.forward ? cd : cv;
+        }
+      }
+      __syncwarp();
+      // Lp <- E_W(L) Lp,  Rp <- Rp E_W(R)   (new values in M, T untouched)
+      for (int o = lane; o < DD; o += 32) {
+        const int x = o / DW, y = o % DW;
+        const int xr = x & ~g.gmask;
+        int ax = 0;
+        for (int a = 0; a < d; a++) ax = (g.gab[a] == (x & g.gmask)) ? a : ax;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int a2 = 0; a2 < d; a2++) acc = cfma(Am[ax * d + a2], Lp[(xr | g.gab[a2]) * DW + y], acc);
+        M[o] = acc;
+      }
+      __syncwarp();
+      for (int o = lane; o < DD; o += 32) Lp[o] = M[o];
+      __syncwarp();
+      for (int o = lane; o < DD; o += 32) {
+        const int x = o / DW, y = o % DW;
+        const int yr = y & ~g.gmask;
+        int by = 0;
+        for (int b = 0; b < d; b++) by = (g.gab[b] == (y & g.gmask)) ? b : by;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int b2 = 0; b2 < d; b2++) acc = cfma(Rp[x * DW + (yr | g.gab[b2])], Vm[b2 * d + by], acc);
+        M[o] = acc;
+      }
+      __syncwarp();
+      for (int o = lane; o < DD; o += 32) Rp[o] = M[o];
+      __syncwarp();
+    }
+    double2 *op = A.ops + (long long)s * A.ops_stride;
+    for (int o = lane; o < DD; o += 32) {
+      op[o] = Lp[o];
+      op[64 + o] = Rp[o];
+    }
+    __syncwarp();
+  }
+}
+
 // vstore <- identity for every (start, VARIABLE gate, direction) slot
 __global__ void k_vstore_identity(double2 *vstore, long long vstride, int S, const int2 *slots,
                                   int nslots) {

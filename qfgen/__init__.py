@@ -254,9 +254,23 @@ def _round(n, p):
     return locs[:p], [VARIABLE] * p, [None] * p
 
 
+def _u3_cnot(n, layers):
+    """The paper's gate set (U3 + CNOT): a VAR U(2) on every qubit,
+    then `layers` x [CNOT(i, i+1), VAR U(2) i, VAR U(2) i+1] down a ladder."""
+    cx = np.eye(4)[[0, 1, 3, 2]]
+    locs, kinds, cm = [(q,) for q in range(n)], [VARIABLE] * n, [None] * n
+    for l in range(layers):
+        i = l % (n - 1)
+        locs += [(i, i + 1), (i,), (i + 1,)]
+        kinds += [CONSTANT, VARIABLE, VARIABLE]
+        cm += [cx, None, None]
+    return locs, kinds, cm
+
+
 def workload(name: str) -> Workload:
     """The configs of BASELINE.json / SURVEY.md Sec. 8d (C1-C5, C2+, C3+) and
-    the NEXT-3 size probes C6 (n = 10) and C7 (n = 12)."""
+    the NEXT-3 size probes C6 (n = 10), C7 (n = 12) and C8 (n = 10, the
+    paper's U3 + CNOT gate set)."""
     if name == "C1":
         l, k, c = _c1()
         return Workload("C1", 2, l, k, c, 4, 10000, "haar", 1,
@@ -293,6 +307,11 @@ def workload(name: str) -> Workload:
         l, k, c = _round(12, 40)
         return Workload("C7", 12, l, k, c, 32, 1000, "self", 9,
                         "12-qubit round of VAR U(4) + U(8) (C5 pattern), 40 gates, self-target, 32 starts")
+    if name == "C8":
+        l, k, c = _u3_cnot(10, 60)
+        return Workload("C8", 10, l, k, c, 256, 1000, "self", 10,
+                        "10-qubit U3+CNOT ladder (10 + 60 x [CNOT, U(2), U(2)] = 190 gates), "
+                        "self-target, 256 starts")
     raise KeyError(name)
 
 
