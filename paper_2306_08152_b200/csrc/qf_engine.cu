@@ -356,6 +356,12 @@ int group_default() {
   return e ? std::max(0, std::min(3, atoi(e))) : 2;
 }
 
+// streaming sweeps replayed as a CUDA graph unless QF_GRAPH=0
+bool graph_default() {
+  const char *e = getenv("QF_GRAPH");
+  return !(e && atoi(e) == 0);
+}
+
 std::vector<StepGroup> make_groups(const qf_circuit_s &c, int umax) {
   std::vector<StepGroup> out;
   StepGroup cur;
@@ -800,8 +806,11 @@ struct Engine {
     return e;
   }
 
-  cudaError_t trace(int it) {
+  int *sweep_index() const { return reinterpret_cast<int *>(ws + L.counters) + 8; }
+
+  cudaError_t trace(int it, const int *it_dev = nullptr) {
     TraceArgs A{};
+    A.it_dev = it_dev;
     A.N = N;
     A.ct = ct();
     A.ct_stride = (long long)N * N;
@@ -1049,6 +1058,79 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   QF_CHECK(E.init_ct());
 
   // ---- a3..a7: sweeps until every start has a verdict
+  // ---- one sweep's launches (a3..a7); replayed from a CUDA graph after the
+  // first sweep: the sequence is the same every sweep (kernels read the
+  // active count and the sweep index from device memory), so the host pays
+  // one graph launch per sweep instead of ~2p kernel launches
+  const int umax = group_default();
+  const std::vector<StepGroup> groups = umax > 0 ? make_groups(c, umax) : std::vector<StepGroup>{};
+  int *it_dev = E.sweep_index();
+  QF_CHECK(cudaMemsetAsync(it_dev, 0, sizeof(int), st));
+  auto sweep_body = [&]() -> cudaError_t {  // everything on E.st (the capture stream swaps in)
+    k_next_sweep<<<1, 1, 0, E.st>>>(it_dev);
+    E.launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (batch && (e = cudaMemsetAsync(E.batch_counts(), 0, 3 * sizeof(unsigned), E.st)) != cudaSuccess)
+      return e;
+    if (!groups.empty()) {
+      for (const auto &G : groups)
+        if ((e = E.group_steps(G)) != cudaSuccess) return e;
+    } else {
+      for (int k = c.p - 1; k >= 0; k--)
+        if ((e = E.step(k, 0)) != cudaSuccess) return e;
+      for (int k = 0; k < c.p; k++)
+        if ((e = E.step(k, 1)) != cudaSuccess) return e;
+    }
+    return E.trace(1, it_dev);  // any sweep >= 1: the index itself comes from it_dev
+  };
+  struct SweepGraph {
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0, sw = 0, env = 0, envb = 0;  // per-sweep stats of the captured sweep
+    ~SweepGraph() {
+      if (exec) cudaGraphExecDestroy(exec);
+    }
+  } sg;
+  const bool graphs = !E.prof.on && graph_default();
+  auto run_sweep = [&](int it) -> cudaError_t {
+    if (!graphs || it < 2) return sweep_body();  // sweep 1 also finishes every lazy setup
+    const int cx = E.ctx;
+    if (!sg.exec) {
+      const long long l0 = E.launches, s0 = E.sw_ctx[cx], e0 = E.env_ctx[cx], b0 = E.env_bytes_ctx[cx];
+      // capture on a private stream (the caller's may be the legacy default
+      // stream, which cannot capture); the replays run on the caller's
+      cudaGraph_t g = nullptr;
+      cudaStream_t cs = nullptr;
+      cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+      E.st = cs;
+      e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        e = sweep_body();
+        const cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+        if (e == cudaSuccess) e = e2;
+      }
+      E.st = st;
+      cudaStreamDestroy(cs);
+      if (e != cudaSuccess) return e;
+      e = cudaGraphInstantiate(&sg.exec, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return e;
+      sg.launches = E.launches - l0;
+      sg.sw = E.sw_ctx[cx] - s0;
+      sg.env = E.env_ctx[cx] - e0;
+      sg.envb = E.env_bytes_ctx[cx] - b0;
+      E.launches = l0;  // the capture ran nothing; the replay below counts
+      E.sw_ctx[cx] = s0;
+      E.env_ctx[cx] = e0;
+      E.env_bytes_ctx[cx] = b0;
+    }
+    E.launches += sg.launches;
+    E.sw_ctx[cx] += sg.sw;
+    E.env_ctx[cx] += sg.env;
+    E.env_bytes_ctx[cx] += sg.envb;
+    return cudaGraphLaunch(sg.exec, st);
+  };
   if (p.max_iters == 0) {
     QF_CHECK(E.trace(0));
   } else if (batch) {
@@ -1057,10 +1139,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     unsigned *h_cnt = reinterpret_cast<unsigned *>(h_flags + p.max_iters + 4);  // 3 words
     for (int it = 1; it <= p.max_iters; it++) {
       E.ctx = it - 1;
-      for (int k = c.p - 1; k >= 0; k--) QF_CHECK(E.step(k, 0));
-      for (int k = 0; k < c.p; k++) QF_CHECK(E.step(k, 1));
-      QF_CHECK(cudaMemsetAsync(E.batch_counts(), 0, 3 * sizeof(unsigned), st));
-      QF_CHECK(E.trace(it));
+      QF_CHECK(run_sweep(it));
       E.ctx = it;
       QF_CHECK(cudaMemcpyAsync(h_cnt, E.batch_counts(), 3 * sizeof(unsigned),
                                cudaMemcpyDeviceToHost, st));
@@ -1085,17 +1164,9 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       if (p.reset_iters > 0 && it % p.reset_iters == 0) QF_CHECK(E.init_ct());
     }
   } else {
-    const int umax = group_default();
-    const std::vector<StepGroup> groups = umax > 0 ? make_groups(c, umax) : std::vector<StepGroup>{};
     for (int it = 1; it <= p.max_iters; it++) {
       E.ctx = it - 1;  // this sweep runs on the starts active after sweep it-1
-      if (!groups.empty()) {
-        for (const auto &G : groups) QF_CHECK(E.group_steps(G));
-      } else {
-        for (int k = c.p - 1; k >= 0; k--) QF_CHECK(E.step(k, 0));
-        for (int k = 0; k < c.p; k++) QF_CHECK(E.step(k, 1));
-      }
-      QF_CHECK(E.trace(it));
+      QF_CHECK(run_sweep(it));
       E.ctx = it;
       if (p.reset_iters > 0 && it % p.reset_iters == 0 && it < p.max_iters) QF_CHECK(E.init_ct());
       QF_CHECK(cudaMemcpyAsync(&h_nact[it], E.n_active(), sizeof(int), cudaMemcpyDeviceToHost, st));

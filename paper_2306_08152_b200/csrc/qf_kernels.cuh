@@ -787,6 +787,7 @@ struct TraceArgs {
   const int *active;
   const int *n_active;
   int it;  // sweep just completed (1-based); 0 = max_iters == 0 call
+  const int *it_dev;  // non-null: the sweep index is read here (CUDA-graph replays)
   double dist_tol, diff_tol_a, diff_tol_r, long_diff_r;
   int long_diff_count, min_iters, max_iters, ring;
   double *hist;   // S x ring
@@ -837,7 +838,7 @@ __global__ void __launch_bounds__(32 * kTraceWarps) k_trace_mask(const TraceArgs
       }
     }
     const double c = 1.0 - hypot(re, im) / (double)A.N;
-    const int it = A.it;
+    const int it = A.it_dev ? *A.it_dev : A.it;
     if (lane == 0) {
       int v = 0;
       if (it == 0) {
@@ -892,6 +893,9 @@ __global__ void __launch_bounds__(32 * kTraceWarps) k_trace_mask(const TraceArgs
     }
   }
 }
+
+// sweep index for graph replays of a sweep (read by k_trace_mask)
+__global__ void k_next_sweep(int *it) { *it += 1; }
 
 // Batch policy: the batch stops after this sweep (the host summed the counts
 // over every shard): each start still running takes its first plateau kind,
