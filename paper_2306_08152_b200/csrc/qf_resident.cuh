@@ -98,19 +98,15 @@ __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
 
 // ct <- E(L) ct E(R) in place for D <= 4, one D x D block (row-rest r,
 // column-rest c) per item held in registers: one shared-memory read and write
-// per element.  `mode` selects the blocks of the pipelined schedule (see
-// k_resident): 0 all, 1 those the next gate's environment reads
-// ((r ^ c) & ~dm == 0), 2 the others; items are spread over threads
-// t0, t0 + nt, ...  No barrier inside.
+// per element; items are spread over threads t0, t0 + nt, ...  No barrier
+// inside.
 template <int D>
 __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N,
-                                    const double2 *Ls, const double2 *Rs, int mode, int dm,
-                                    int t0, int nt) {
+                                    const double2 *Ls, const double2 *Rs, int t0, int nt) {
   constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
   const int lnr = n - LD, NR = 1 << lnr;  // N / D rests (no runtime division)
   for (int it = t0; it < NR * NR; it += nt) {
     const int r = it >> lnr, c = it & (NR - 1);
-    if (mode != 0 && (((r ^ c) & ~dm) == 0) != (mode == 1)) continue;
     const int rb = rspread(g, n, r), cb = rspread(g, n, c);
     double2 x[D][D];
 #pragma unroll
@@ -118,9 +114,7 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
 #pragma unroll
       for (int b = 0; b < D; b++) x[a][b] = ct[sidx(rb | g.abits[a], cb | g.abits[b], N)];
     // row by row: z[a][:] = (L[a][:] x) R, stored over the (register-held)
-    // block.  The outputs go in pairs: a store may alias the next R loads
-    // for the compiler, so a pair gives it four independent accumulation
-    // chains to interleave instead of two
+    // block, the outputs in pairs (four independent accumulation chains)
 #pragma unroll
     for (int a = 0; a < D; a++) {
       double2 y[D];
@@ -351,18 +345,16 @@ __device__ __forceinline__ void res_prepare(const ResidentArgs &A, const ResView
   }
 }
 
-// sandwich of gate g with operands (Lb, Rb); mode/dm/t0/nt as in
-// res_sandwich_blocks.  d = 8 (two-phase, internal barriers) only with mode 0
-// and all threads.
+// sandwich of gate g with operands (Lb, Rb); t0/nt as in
+// res_sandwich_blocks.  d = 8 (two-phase, internal barriers): all threads.
 template <int MAXD>
 __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResView &V,
-                                          const double2 *Lb, const double2 *Rb, int mode, int dm,
-                                          int t0, int nt) {
+                                          const double2 *Lb, const double2 *Rb, int t0, int nt) {
   if (g.d == 2) {
-    res_sandwich_blocks<2>(ct, g, V.n, V.N, Lb, Rb, mode, dm, t0, nt);
+    res_sandwich_blocks<2>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, mode, dm, t0, nt);
+      res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
     } else if constexpr (MAXD >= 8) {
       res_sandwich<8>(ct, g, V.n, V.N, Lb, Rb);
     }
@@ -412,13 +404,6 @@ __device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
 }
 
 // rest-index bits (of gate g) that belong to the location `next_mask`
-__device__ __forceinline__ int rest_bits_in(const GateDesc &g, int n, int next_mask) {
-  int dm = 0;
-#pragma unroll
-  for (int k = 0; k < kMaxQubits; k++)
-    if (k < n - g.m && ((next_mask >> g.rest_pos[k]) & 1)) dm |= 1 << k;
-  return dm;
-}
 
 // Schedule of one TwoSidedSweep as 2p steps: j < p -> (gate p-1-j, backward),
 // j >= p -> (gate j-p, forward).  Step j's operands live in buffer j & 1.
@@ -534,7 +519,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
 #ifdef QF_POLAR_COUNT
           const long long c0 = clock64();
 #endif
-          res_apply<MAXD>(ct, g, V, Lb + buf, Rb + buf, 0, 0, tid, nt);
+          res_apply<MAXD>(ct, g, V, Lb + buf, Rb + buf, tid, nt);
           __syncthreads();
 #ifdef QF_POLAR_COUNT
           const long long c1 = clock64();
