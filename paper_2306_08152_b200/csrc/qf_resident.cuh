@@ -345,16 +345,22 @@ __device__ __forceinline__ void res_prepare(const ResidentArgs &A, const ResView
   }
 }
 
-// sandwich of gate g with operands (Lb, Rb); t0/nt as in
-// res_sandwich_blocks.  d = 8 (two-phase, internal barriers): all threads.
+// sandwich of gate g with operands (Lb, Rb), all threads.  Register blocks
+// when there are at least as many d x d blocks as threads; otherwise (small n:
+// e.g. 4 blocks for a 4 x 4 gate at n = 3) the two-phase form, whose column /
+// row items keep every lane busy (fewer, shorter dependent chains), as for d = 8.
 template <int MAXD>
 __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResView &V,
                                           const double2 *Lb, const double2 *Rb, int t0, int nt) {
+  const int nb = V.N / g.d;
+  const bool blocks = nb * nb >= nt;
   if (g.d == 2) {
-    res_sandwich_blocks<2>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+    if (blocks) res_sandwich_blocks<2>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+    else res_sandwich<2>(ct, g, V.n, V.N, Lb, Rb);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+      if (blocks) res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+      else res_sandwich<4>(ct, g, V.n, V.N, Lb, Rb);
     } else if constexpr (MAXD >= 8) {
       res_sandwich<8>(ct, g, V.n, V.N, Lb, Rb);
     }
