@@ -1041,7 +1041,11 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     const size_t smem = (size_t)N * N * 16 + 8 * 64 * 16;
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
-    auto kern = maxm == 1 ? k_resident<2, false> : maxm == 2 ? k_resident<4, false> : k_resident<8, false>;
+    const bool small = c.n <= 4;
+    auto kern = small ? (maxm == 1 ? k_resident<2, false, true> : maxm == 2 ? k_resident<4, false, true>
+                                                                           : k_resident<8, false, true>)
+                      : (maxm == 1 ? k_resident<2, false> : maxm == 2 ? k_resident<4, false>
+                                                                     : k_resident<8, false>);
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
@@ -1459,7 +1463,11 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
   A.R = 0;
   const int threads = resident_threads(maxn);
   const size_t smem = (size_t)A.N * A.N * 16 + 8 * 64 * 16;
-  auto kern = maxm == 1 ? k_resident<2, true> : maxm == 2 ? k_resident<4, true> : k_resident<8, true>;
+  const bool small = maxn <= 4;
+  auto kern = small ? (maxm == 1 ? k_resident<2, true, true> : maxm == 2 ? k_resident<4, true, true>
+                                                                         : k_resident<8, true, true>)
+                    : (maxm == 1 ? k_resident<2, true> : maxm == 2 ? k_resident<4, true>
+                                                                   : k_resident<8, true>);
   QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));

@@ -349,11 +349,11 @@ __device__ __forceinline__ void res_prepare(const ResidentArgs &A, const ResView
 // when there are at least as many d x d blocks as threads; otherwise (small n:
 // e.g. 4 blocks for a 4 x 4 gate at n = 3) the two-phase form, whose column /
 // row items keep every lane busy (fewer, shorter dependent chains), as for d = 8.
-template <int MAXD>
+template <int MAXD, bool SMALL = false>
 __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResView &V,
                                           const double2 *Lb, const double2 *Rb, int t0, int nt) {
   const int nb = V.N / g.d;
-  const bool blocks = nb * nb >= nt;
+  const bool blocks = !SMALL && nb * nb >= nt;
   if (g.d == 2) {
     if (blocks) res_sandwich_blocks<2>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
     else res_sandwich<2>(ct, g, V.n, V.N, Lb, Rb);
@@ -418,8 +418,10 @@ __device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
 // MULTI: the launch holds several problems (NEXT-2): each start finds its
 // problem in A.probs (gate tables in global memory); otherwise the single
 // problem's gate table is read from the kernel parameters.
-template <int MAXD, bool MULTI>
-__global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ ResidentArgs A) {
+// SMALL (every problem n <= 4): the two-phase sandwich only -- no register
+// block path, far fewer registers, more CTAs (starts) per SM.
+template <int MAXD, bool MULTI, bool SMALL = false>
+__global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(const __grid_constant__ ResidentArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
   double2 *ct = reinterpret_cast<double2 *>(smraw);
   double2 *Lb = ct + A.N * A.N;  // [2][64]; A.N = the largest N of the launch
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(128, 3) k_resident(const __grid_constant__ Res
 #ifdef QF_POLAR_COUNT
           const long long c0 = clock64();
 #endif
-          res_apply<MAXD>(ct, g, V, Lb + buf, Rb + buf, tid, nt);
+          res_apply<MAXD, SMALL>(ct, g, V, Lb + buf, Rb + buf, tid, nt);
           __syncthreads();
 #ifdef QF_POLAR_COUNT
           const long long c1 = clock64();
