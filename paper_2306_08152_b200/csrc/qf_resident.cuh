@@ -317,13 +317,12 @@ __device__ void res_prepare_d(const ResidentArgs &A, const ResView &V, const dou
       Lb[e] = forward ? Pm[e] : od;
       Rb[e] = forward ? od : Pm[e];
     }
-  } else {
-    const double2 *cm = V.cmats + g.goff;
+  } else {  // CONSTANT: its matrix was staged in Uo
     for (int e = lane; e < DD; e += 32) {
       const int i = e / D, k = e % D;
-      const double2 cd = cconj(cm[k * D + i]);
-      Lb[e] = forward ? cm[e] : cd;
-      Rb[e] = forward ? cd : cm[e];
+      const double2 cd = cconj(Uo[k * D + i]);
+      Lb[e] = forward ? Uo[e] : cd;
+      Rb[e] = forward ? cd : Uo[e];
     }
   }
   __syncwarp();
@@ -500,6 +499,14 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
           }
         }
         __syncthreads();
+      } else if (serial) {  // CONSTANT: its matrix into Uo (prefetched when `pre`)
+        const double2 *cm = V.cmats + g2.goff;
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+          const int e = lane + 32 * q;
+          if (e < g2.d * g2.d) Uo[e] = pre ? upf[q] : cm[e];
+        }
+        __syncwarp();
       }
       if (serial) res_prepare<MAXD>(A, V, ct, g2, s, fw2, Lb + off, Rb + off, Uo, Pm, Am, Vm, lane);
       __syncthreads();
@@ -515,8 +522,8 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
           if (has_next && serial) {  // prefetch u_old of the next gate (L2 latency
             int fw2;                 // hidden behind this sandwich)
             const GateDesc &g2 = gdesc[gate_of(j + 1, fw2)];
-            if (g2.kind != 1) {
-              const double2 *u2 = V.u0 + g2.goff;
+            {  // u_old (VARIABLE, RZ) or the fixed matrix (CONSTANT)
+              const double2 *u2 = (g2.kind != 1 ? V.u0 : V.cmats) + g2.goff;
 #pragma unroll
               for (int q = 0; q < 2; q++) {
                 const int e = lane + 32 * q;
