@@ -262,27 +262,30 @@ template <int D>
 __device__ void warp_polar_jacobi(double2 *Am, double2 *Vm, double2 *U, int lane,
                                   const double2 *v0 = nullptr) {
   if constexpr (D == 2) {
-    if (lane == 0) {
+    // closed form on lanes 0..3 (one output each), two rsqrt on the chain:
+    // U = (A + (det/|det|) adj(A)^H) / sqrt(||A||_F^2 + 2 |det A|)
+    if (lane < 4) {
       const double2 a = Am[0], b = Am[1], c = Am[2], e = Am[3];
       const double2 det = make_double2(a.x * e.x - a.y * e.y - (b.x * c.x - b.y * c.y),
                                        a.x * e.y + a.y * e.x - (b.x * c.y + b.y * c.x));
-      const double adet = hypot(det.x, det.y);
-      const double2 ph = adet > 0.0 ? make_double2(det.x / adet, det.y / adet)
-                                    : make_double2(1.0, 0.0);
-      const double nrm = sqrt(cabs2(a) + cabs2(b) + cabs2(c) + cabs2(e) + 2.0 * adet);
-      if (nrm > 0.0) {
-        const double inv = 1.0 / nrm;
+      const double d2 = cabs2(det);
+      const double rinv = d2 > 0.0 ? rsqrt(d2) : 0.0;        // 1 / |det|
+      const double2 ph = d2 > 0.0 ? cscale(det, rinv) : make_double2(1.0, 0.0);
+      const double s2 = cabs2(a) + cabs2(b) + cabs2(c) + cabs2(e) + 2.0 * (d2 * rinv);
+      double2 out;
+      if (s2 > 0.0) {
+        const double inv = rsqrt(s2);
         // adj(A)^H = [[conj e, -conj c], [-conj b, conj a]]
-        U[0] = cscale(cadd(a, cmul(ph, cconj(e))), inv);
-        U[1] = cscale(cadd(b, cmul(ph, make_double2(-c.x, c.y))), inv);
-        U[2] = cscale(cadd(c, cmul(ph, make_double2(-b.x, b.y))), inv);
-        U[3] = cscale(cadd(e, cmul(ph, cconj(a))), inv);
+        const double2 src = lane == 0 ? a : lane == 1 ? b : lane == 2 ? c : e;
+        const double2 adj = lane == 0 ? cconj(e)
+                            : lane == 1 ? make_double2(-c.x, c.y)
+                            : lane == 2 ? make_double2(-b.x, b.y)
+                                        : cconj(a);
+        out = cscale(cadd(src, cmul(ph, adj)), inv);
       } else {
-        U[0] = make_double2(1.0, 0.0);
-        U[1] = make_double2(0.0, 0.0);
-        U[2] = make_double2(0.0, 0.0);
-        U[3] = make_double2(1.0, 0.0);
+        out = make_double2(lane == 0 || lane == 3 ? 1.0 : 0.0, 0.0);
       }
+      U[lane] = out;
     }
     __syncwarp();
   } else {
