@@ -499,12 +499,12 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
           }
         }
         __syncthreads();
-      } else if (serial) {  // CONSTANT: its matrix into Uo (prefetched when `pre`)
+      } else if (serial) {  // CONSTANT: its matrix into Uo (prefetched when SMALL and `pre`)
         const double2 *cm = V.cmats + g2.goff;
 #pragma unroll
         for (int q = 0; q < 2; q++) {
           const int e = lane + 32 * q;
-          if (e < g2.d * g2.d) Uo[e] = pre ? upf[q] : cm[e];
+          if (e < g2.d * g2.d) Uo[e] = (SMALL && pre) ? upf[q] : cm[e];
         }
         __syncwarp();
       }
@@ -522,7 +522,10 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
           if (has_next && serial) {  // prefetch u_old of the next gate (L2 latency
             int fw2;                 // hidden behind this sandwich)
             const GateDesc &g2 = gdesc[gate_of(j + 1, fw2)];
-            {  // u_old (VARIABLE, RZ) or the fixed matrix (CONSTANT)
+            // u_old (VARIABLE, RZ); for SMALL launches, whose steps are short,
+            // also the fixed matrix of a CONSTANT gate (measured 1 % slower at
+            // n = 6, so not there)
+            if (SMALL || g2.kind != 1) {
               const double2 *u2 = (g2.kind != 1 ? V.u0 : V.cmats) + g2.goff;
 #pragma unroll
               for (int q = 0; q < 2; q++) {

@@ -1,0 +1,36 @@
+"""A/B timing of library builds on one box: python tools/ab_lib.py LIB_A LIB_B [reps]
+(C4, 3 sweeps, resident engine; alternates the builds to cancel drift)."""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+libs = sys.argv[1:3]
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+code = r'''
+import sys, os
+sys.path.insert(0, %r)
+from paper_2306_08152_b200 import _build
+_build.LIB = sys.argv[1]
+import numpy as np, torch
+import paper_2306_08152_b200 as qf, qfgen
+w = qfgen.workload(sys.argv[2] if len(sys.argv) > 2 else "C4")
+dev = torch.device("cuda:0")
+c = qf.Circuit.from_workload(w)
+dV = torch.from_numpy(np.ascontiguousarray(w.target_unitary())).to(dev)
+dI = torch.from_numpy(w.initial()).to(dev)
+ws = torch.empty(qf.qf_workspace_size(c, w.starts, max_iters=3), dtype=torch.uint8, device=dev)
+ms = []
+for _ in range(3):
+    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=3, profile=1, engine=qf.QF_ENGINE_RESIDENT)
+    ms.append(r.stats["resident_ms"])
+print(min(ms[1:]))
+''' % ROOT
+res = {l: [] for l in libs}
+for _ in range(reps):
+    for l in libs:
+        out = subprocess.run([sys.executable, "-c", code, l], capture_output=True, text=True)
+        res[l].append(float(out.stdout.strip().split()[-1]))
+for l in libs:
+    print(os.path.basename(l), " ".join(f"{x:.2f}" for x in res[l]), "min", f"{min(res[l]):.2f}")
