@@ -1,13 +1,25 @@
-"""A/B timing of library builds on one box: python tools/ab_lib.py LIB_A LIB_B [reps]
-(C4, 3 sweeps, resident engine; alternates the builds to cancel drift)."""
+"""A/B timing of library builds / switches on one box:
+  python tools/ab_lib.py SPEC_A SPEC_B [SPEC_C ...] [--reps R] [--config C]
+SPEC = path/to/lib.so[@VAR=value[,VAR=value]] (environment for that arm).
+C4 (or `config`), 3 sweeps, resident engine; alternates the arms to cancel
+drift and prints each run's k_resident time (ms)."""
 import ctypes
 import os
 import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-libs = sys.argv[1:3]
-reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+args = sys.argv[1:]
+reps, cfg = 3, "C4"
+if "--reps" in args:
+    i = args.index("--reps")
+    reps = int(args[i + 1])
+    del args[i:i + 2]
+if "--config" in args:
+    i = args.index("--config")
+    cfg = args[i + 1]
+    del args[i:i + 2]
+libs = args
 code = r'''
 import sys, os
 sys.path.insert(0, %r)
@@ -30,7 +42,13 @@ print(min(ms[1:]))
 res = {l: [] for l in libs}
 for _ in range(reps):
     for l in libs:
-        out = subprocess.run([sys.executable, "-c", code, l], capture_output=True, text=True)
+        path, _, envs = l.partition("@")
+        env = dict(os.environ)
+        for kv in filter(None, envs.split(",")):
+            k, _, v = kv.partition("=")
+            env[k] = v
+        out = subprocess.run([sys.executable, "-c", code, path, cfg], capture_output=True, text=True,
+                             env=env)
         res[l].append(float(out.stdout.strip().split()[-1]))
 for l in libs:
-    print(os.path.basename(l), " ".join(f"{x:.2f}" for x in res[l]), "min", f"{min(res[l]):.2f}")
+    print(l, " ".join(f"{x:.2f}" for x in res[l]), "min", f"{min(res[l]):.2f}")
