@@ -238,6 +238,11 @@ qf_status qf_instantiate_device(qf_circuit_t c, const double *d_target,
 qf_status qf_result_get(qf_result_t r, int start, double *delta, int *iters,
                         int *verdict, double *gates);
 int qf_result_best(qf_result_t r);
+/* Bulk copies: every start's summary (count = num_starts records of 16 B) and,
+ * for host calls, every start's packed gates (num_starts x var_doubles
+ * doubles; QF_E_ARG for device calls, which hold only the best start's). */
+qf_status qf_result_summaries(qf_result_t r, qf_summary *out, int64_t count);
+qf_status qf_result_gates(qf_result_t r, double *out, int64_t count);
 int qf_result_num_starts(qf_result_t r);
 /* record index i in [0, record_count): costs[R] (NaN past the last sweep),
  * gates_per_sweep[R * var_doubles] (nullable); *len = min(R, sweeps). */

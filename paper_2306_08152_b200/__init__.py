@@ -36,6 +36,7 @@ EXPORTS = [
     "qf_result_get", "qf_result_best", "qf_result_num_starts", "qf_result_trace",
     "qf_result_stats", "qf_result_destroy", "qf_select_best_device", "qf_select_best_host",
     "qf_last_error", "qf_version", "qf_instantiate_many", "qf_unitary_to_u3",
+    "qf_result_summaries", "qf_result_gates",
 ]
 
 
@@ -147,6 +148,8 @@ def _declare(L):
     L.qf_instantiate_many.argtypes = [c.c_int32, c.POINTER(_VP), c.POINTER(_D), c.POINTER(_D),
                                       _I, c.POINTER(qf_params), c.POINTER(_VP)]
     L.qf_unitary_to_u3.argtypes = [_D, _D]
+    L.qf_result_summaries.argtypes = [_VP, _VP, c.c_int64]
+    L.qf_result_gates.argtypes = [_VP, _D, c.c_int64]
     L.qf_last_error.restype = c.c_char_p
     L.qf_last_error.argtypes = []
     L.qf_version.restype = c.c_char_p
@@ -248,17 +251,17 @@ def _collect(h, var, all_gates) -> Result:
     L = lib()
     S = L.qf_result_num_starts(h)
     summ = np.zeros(S, dtype=SUMMARY_DTYPE)
-    d = ctypes.c_double()
-    it = ctypes.c_int()
-    v = ctypes.c_int()
-    gates = np.zeros((S if all_gates else 1, var))
-    for s in range(S):
-        g = gates[s].ctypes.data_as(_D) if (all_gates and var) else None
-        _check(L.qf_result_get(h, s, ctypes.byref(d), ctypes.byref(it), ctypes.byref(v), g))
-        summ[s] = (d.value, it.value, v.value)
+    if S:
+        _check(L.qf_result_summaries(h, _VP(summ.ctypes.data), S))
     best = L.qf_result_best(h)
-    if not all_gates and var:
-        _check(L.qf_result_get(h, -1, None, None, None, gates[0].ctypes.data_as(_D)))
+    if all_gates:
+        gates = np.zeros((S, var))
+        if S and var:
+            _check(L.qf_result_gates(h, gates.ctypes.data_as(_D), S * var))
+    else:
+        gates = np.zeros((1, var))
+        if var and best >= 0:
+            _check(L.qf_result_get(h, -1, None, None, None, gates[0].ctypes.data_as(_D)))
     st = qf_stats()
     _check(L.qf_result_stats(h, ctypes.byref(st)))
     stats = {f: getattr(st, f) for f, _ in qf_stats._fields_}

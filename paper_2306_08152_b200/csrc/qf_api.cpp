@@ -387,6 +387,24 @@ qf_status qf_result_get(qf_result_t r, int start, double *delta, int *iters, int
 
 int qf_result_best(qf_result_t r) { return r ? r->best : -1; }
 
+qf_status qf_result_summaries(qf_result_t r, qf_summary *out, int64_t count) {
+  qf::g_err.clear();
+  if (!r || !out) return fail(QF_E_ARG, "result and out must not be NULL");
+  if (count != r->num_starts) return fail(QF_E_ARG, "count must equal num_starts");
+  if (count > 0) std::memcpy(out, r->summary.data(), (size_t)count * sizeof(qf_summary));
+  return QF_OK;
+}
+
+qf_status qf_result_gates(qf_result_t r, double *out, int64_t count) {
+  qf::g_err.clear();
+  if (!r || !out) return fail(QF_E_ARG, "result and out must not be NULL");
+  if (!r->all_gates) return fail(QF_E_ARG, "a device call holds only the best start's gates");
+  if (count != (int64_t)r->num_starts * r->var_doubles)
+    return fail(QF_E_ARG, "count must equal num_starts * var_doubles");
+  if (count > 0) std::memcpy(out, r->gates.data(), (size_t)count * 8);
+  return QF_OK;
+}
+
 int qf_result_num_starts(qf_result_t r) { return r ? r->num_starts : 0; }
 
 qf_status qf_result_trace(qf_result_t r, int i, double *costs, double *gates_per_sweep, int *len) {

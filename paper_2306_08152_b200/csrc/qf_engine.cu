@@ -961,11 +961,21 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   QF_CHECK(cudaGetLastError());
   // pinned host words: [0] input flags, [1 + j] = n_active after sweep j
   int *h_flags = nullptr;
-  QF_CHECK(cudaHostAlloc(&h_flags, ((size_t)p.max_iters + 8) * sizeof(int), cudaHostAllocDefault));
+  // pinned words from the recycled pool (a fresh cudaHostAlloc per call costs
+  // more than a whole small instantiation)
+  size_t h_cap = 0;
+  bool h_pinned = false;
+  h_flags = static_cast<int *>(pinned_get(((size_t)p.max_iters + 8) * sizeof(int), &h_cap, &h_pinned));
+  if (!h_flags) {
+    set_error("host allocation failed");
+    return QF_E_OOM;
+  }
   struct Pinned {
     int *p;
-    ~Pinned() { cudaFreeHost(p); }
-  } pinned{h_flags};
+    size_t cap;
+    bool pinned;
+    ~Pinned() { pinned_put(p, cap, pinned); }
+  } pinned{h_flags, h_cap, h_pinned};
   int *h_nact = h_flags + 1;
   h_nact[0] = S;
   QF_CHECK(cudaMemcpyAsync(h_flags, E.bad(), sizeof(int), cudaMemcpyDeviceToHost, st));
