@@ -144,11 +144,28 @@ __global__ void __launch_bounds__(kTileItems)
   int jt_c2 = 0;
   for (int k = 0; k < A.log_ct; k++) jt_c2 |= ((cl2 >> k) & 1) << A.jt_rest[k];
 
-  int cur = -1;
-  for (long long t = t0; t < t1; t++) {
+  // tile t -> (start, row base, column base); the next tile's column vector
+  // is loaded into registers while this tile is in phases 2-3
+  auto tile_at = [&](long long t, int &s, int &rbase, int &cbase) {
     const int ai = (int)(t / A.tiles_per_start);
     const int tt = (int)(t - (long long)ai * A.tiles_per_start);
-    const int s = A.active[ai];
+    s = A.active[ai];
+    const int tr = tt / A.TC, tc = tt - (tt / A.TC) * A.TC;
+    rbase = spread_rest(A.b, tr * A.RT) | row1;
+    cbase = spread_rest(A.b, tc * A.CT) | col1;
+  };
+  double2 x[D];
+  int s = 0, rbase = 0, cbase = 0;
+  if (t0 < t1) {
+    tile_at(t0, s, rbase, cbase);
+    if (tid < items) {
+      const double2 *cts = A.ct + (long long)s * A.ct_stride;
+#pragma unroll
+      for (int a = 0; a < D; a++) x[a] = cts[(long long)(rbase | A.b.abits[a]) * N + cbase];
+    }
+  }
+  int cur = -1;
+  for (long long t = t0; t < t1; t++) {
     if (s != cur) {  // CTA-uniform branch
       __syncthreads();  // previous tile done with Ls / Rs
       if (tid < D * D) {
@@ -163,16 +180,10 @@ __global__ void __launch_bounds__(kTileItems)
       cur = s;
       __syncthreads();
     }
-    const int tr = tt / A.TC, tc = tt - (tt / A.TC) * A.TC;
-    const int rbase = spread_rest(A.b, tr * A.RT) | row1;
-    const int cbase = spread_rest(A.b, tc * A.CT) | col1;
     double2 *cts = A.ct + (long long)s * A.ct_stride;
+    const int rb0 = rbase, cb0 = cbase;
+    double2 y[D];
     if (tid < items) {
-      double2 x[D];
-#pragma unroll
-      for (int a = 0; a < D; a++)
-        x[a] = cts[(long long)(rbase | A.b.abits[a]) * N + cbase];
-      double2 y[D];
 #pragma unroll
       for (int a = 0; a < D; a++) {
         double2 acc = make_double2(0.0, 0.0);
@@ -185,8 +196,16 @@ __global__ void __launch_bounds__(kTileItems)
         for (int a = 0; a < D; a++) tile[(rl1 * D + a) * A.DC + jt1] = y[a];
       } else {
 #pragma unroll
-        for (int a = 0; a < D; a++)
-          cts[(long long)(rbase | A.b.abits[a]) * N + cbase] = y[a];
+        for (int a = 0; a < D; a++) cts[(long long)(rb0 | A.b.abits[a]) * N + cb0] = y[a];
+      }
+    }
+    // prefetch the next tile's column vector (its loads overlap phases 2-3)
+    if (t + 1 < t1) {
+      tile_at(t + 1, s, rbase, cbase);
+      if (tid < items) {
+        const double2 *ctn = A.ct + (long long)s * A.ct_stride;
+#pragma unroll
+        for (int a = 0; a < D; a++) x[a] = ctn[(long long)(rbase | A.b.abits[a]) * N + cbase];
       }
     }
     if (has_r) {
@@ -208,8 +227,7 @@ __global__ void __launch_bounds__(kTileItems)
       if (tid < items) {
 #pragma unroll
         for (int a = 0; a < D; a++)
-          cts[(long long)(rbase | A.b.abits[a]) * N + cbase] =
-              tile[(rl1 * D + a) * A.DC + jt1];
+          cts[(long long)(rb0 | A.b.abits[a]) * N + cb0] = tile[(rl1 * D + a) * A.DC + jt1];
       }
       __syncthreads();
     }

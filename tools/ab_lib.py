@@ -1,8 +1,9 @@
 """A/B timing of library builds / switches on one box:
   python tools/ab_lib.py SPEC_A SPEC_B [SPEC_C ...] [--reps R] [--config C]
 SPEC = path/to/lib.so[@VAR=value[,VAR=value]] (environment for that arm).
-C4 (or `config`), 3 sweeps, resident engine; alternates the arms to cancel
-drift and prints each run's k_resident time (ms)."""
+C4 (or `config`), 3 sweeps, resident engine (AB_ENGINE=stream for the
+streaming one); alternates the arms to cancel drift and prints each run's
+wall time of the whole call (ms, best of the last two of three)."""
 import ctypes
 import os
 import subprocess
@@ -33,10 +34,15 @@ c = qf.Circuit.from_workload(w)
 dV = torch.from_numpy(np.ascontiguousarray(w.target_unitary())).to(dev)
 dI = torch.from_numpy(w.initial()).to(dev)
 ws = torch.empty(qf.qf_workspace_size(c, w.starts, max_iters=3), dtype=torch.uint8, device=dev)
+eng = {"stream": qf.QF_ENGINE_STREAM, "resident": qf.QF_ENGINE_RESIDENT}[os.environ.get("AB_ENGINE", "resident")]
+import time
 ms = []
 for _ in range(3):
-    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=3, profile=1, engine=qf.QF_ENGINE_RESIDENT)
-    ms.append(r.stats["resident_ms"])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=3, engine=eng, want_result=False)
+    torch.cuda.synchronize()
+    ms.append(1e3 * (time.perf_counter() - t0))
 print(min(ms[1:]))
 ''' % ROOT
 res = {l: [] for l in libs}
