@@ -346,14 +346,18 @@ struct StepGroup {
   std::vector<std::pair<int, int>> steps;  // (gate, forward)
 };
 
-// NEXT-3 grouped steps on the streaming engine, groups of <= umax qubits:
-// default 2 (a group then flushes with the HBM-bound d <= 4 kernels; measured
-// 2.0x on the U3 + CNOT template C8, neutral on ladders); QF_GROUP=3 also
-// forms 3-qubit groups (d = 8 flush, FP64-bound: +15 % on C5, 0 on C6),
-// QF_GROUP=0 runs one pass per step
-int group_default() {
+// NEXT-3 grouped steps on the streaming engine, groups of <= umax qubits.
+// Default: 2 (a group then flushes with the HBM-bound d <= 4 kernels;
+// measured 2.0x on the U3 + CNOT template C8, where 3 is 6 % slower), or 3
+// when the template already has 3-qubit gates and n <= 9 (its d = 8 flushes
+// then use the row-tile kernel: +15 % on C5; at n >= 10 the tile kernel makes
+// it a wash, C6).  QF_GROUP=0..3 overrides (0: one pass per step).
+int group_default(const qf_circuit_s &c) {
   const char *e = getenv("QF_GROUP");
-  return e ? std::max(0, std::min(3, atoi(e))) : 2;
+  if (e) return std::max(0, std::min(3, atoi(e)));
+  bool has3 = false;
+  for (int k = 0; k < c.p; k++) has3 |= c.arity[k] == 3;
+  return (has3 && c.n <= kRowsMaxQubits) ? 3 : 2;
 }
 
 // streaming sweeps replayed as a CUDA graph unless QF_GRAPH=0
@@ -428,7 +432,7 @@ struct Engine {
     if (p.profile) prof.init();
     if (const char *e = getenv("QF_SANDWICH")) {
       const std::string v(e);
-      sw_kind = v == "rows" ? 1 : v == "tile" ? 2 : v == "reg" ? 3 : 0;
+      sw_kind = v == "rows" ? 1 : v == "tile" ? 2 : v == "reg" ? 3 : v == "regtile" ? 4 : 0;
     }
     if (const char *e = getenv("QF_WARM")) warm = std::string(e) == "1";
     if (const char *e = getenv("QF_POLAR")) polar_jacobi = std::string(e) == "jacobi";
@@ -585,6 +589,7 @@ struct Engine {
     const bool rows_ok = c.n <= kRowsMaxQubits && row_tiles(c.n, A.b.m).first * A.b.d <= 32;
     int kind = sw_kind;
     if (kind == 0) kind = A.b.d <= 4 ? 3 : (rows_ok ? 1 : 2);
+    if (kind == 4) kind = A.b.d <= 4 ? 3 : 2;  // register blocks, tile kernel for d = 8
     if (kind == 3 && A.b.d > 4) kind = rows_ok ? 1 : 2;
     if (kind == 1 && !rows_ok) kind = 2;
     if (kind == 3) return A.b.d == 2 ? launch_reg<2>(A) : launch_reg<4>(A);
@@ -1076,7 +1081,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   // first sweep: the sequence is the same every sweep (kernels read the
   // active count and the sweep index from device memory), so the host pays
   // one graph launch per sweep instead of ~2p kernel launches
-  const int umax = group_default();
+  const int umax = group_default(c);
   const std::vector<StepGroup> groups = umax > 0 ? make_groups(c, umax) : std::vector<StepGroup>{};
   int *it_dev = E.sweep_index();
   QF_CHECK(cudaMemsetAsync(it_dev, 0, sizeof(int), st));
