@@ -219,7 +219,9 @@ def roofline(st, step_ms, w):
     peak, src = load_peaks()
     ach = (sw_bytes / 1e9) / (sw_ms / 1e3) if sw_ms > 0 else None
     traffic, _ = load_traffic(w.name)
-    return {"kernel": "k_sandwich_rows" if w.n <= 9 else "k_sandwich", "bound": "hbm",
+    return {"kernel": ("sandwich passes (k_sandwich_reg d<=4, " +
+                       ("k_sandwich_rows" if w.n <= 9 else "k_sandwich") + " d=8), aggregate"),
+            "bound": "hbm",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak if ach else None,
             "traffic": traffic, "alg_bytes_per_launch": sw_bytes / sw_n if sw_n else None,
             "launches": sw_n, "avg_launch_us": 1e3 * sw_ms / sw_n if sw_n else None,
