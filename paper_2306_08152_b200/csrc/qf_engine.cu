@@ -1578,6 +1578,27 @@ qf_status select_best_device(const qf_summary *d, long long count, cudaStream_t 
 
 }  // namespace qf
 
+// Host logic of NEXT-3 exposed for CPU tests (not part of qf.h): the step
+// groups of a template as flat int records [w, qubits of W (w), nsteps,
+// (gate, forward) x nsteps] ...; returns the ints written, -1 if cap is short.
+extern "C" int qf_debug_groups(const qf_circuit_s *c, int umax, int *out, int cap) {
+  if (!c || !out) return -1;
+  const std::vector<qf::StepGroup> g = qf::make_groups(*c, umax);
+  int o = 0;
+  for (const auto &G : g) {
+    const int need = 2 + (int)G.wq.size() + 2 * (int)G.steps.size();
+    if (o + need > cap) return -1;
+    out[o++] = (int)G.wq.size();
+    for (int q : G.wq) out[o++] = q;
+    out[o++] = (int)G.steps.size();
+    for (const auto &st : G.steps) {
+      out[o++] = st.first;
+      out[o++] = st.second;
+    }
+  }
+  return o;
+}
+
 #ifdef QF_POLAR_COUNT
 // debug build only (tools/polar_stats.py): polar-factor iteration counters
 extern "C" void qf_debug_polar_counts(unsigned long long *out) {
