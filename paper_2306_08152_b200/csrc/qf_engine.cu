@@ -220,7 +220,7 @@ std::pair<int, int> row_tiles(int n, int m) {
 struct Layout {
   size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
       rec_slot, rec_starts, rec_cost, rec_gates, summary, best, part, tpart, vstore, vslots,
-      gdesc, plat, gops, total;
+      gdesc, plat, gops, bcnt, total;
   long long vstride;  // complex per start in vstore (sum over VARIABLE gates of 2 d^2)
   int nvslots;
   int ring;
@@ -273,6 +273,7 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
   L.gdesc = take((size_t)std::max(1, c.p) * sizeof(GateDesc));
   L.plat = take(S * 4);
   L.gops = take(S * 128 * 16);  // grouped steps: Lp, Rp (<= 8 x 8) per start
+  L.bcnt = take((3 * ((size_t)std::max(0, p.max_iters) + 1) + 2) * 4);  // resident batch counts
   L.total = o;
   return L;
 }
@@ -862,6 +863,21 @@ struct Engine {
 
 }  // namespace
 
+// the single-problem resident kernel for n qubits and largest arity maxm
+using ResidentKernel = void (*)(ResidentArgs);
+ResidentKernel resident_kernel(int n, int maxm) {
+  if (n <= 4)
+    return maxm == 1 ? k_resident<2, false, true> : maxm == 2 ? k_resident<4, false, true>
+                                                            : k_resident<8, false, true>;
+  return maxm == 1 ? k_resident<2, false> : maxm == 2 ? k_resident<4, false> : k_resident<8, false>;
+}
+
+// batch policy on the resident engine when the batch fits (QF_RES_BATCH=0: streaming)
+bool resident_batch_default() {
+  const char *e = getenv("QF_RES_BATCH");
+  return !(e && atoi(e) == 0);
+}
+
 // gate descriptors of the resident engine (voff: warm-start slots or null)
 std::vector<GateDesc> make_gdesc(const qf_circuit_s &c, const std::vector<int> *voff) {
   std::vector<GateDesc> gd(c.p);
@@ -996,7 +1012,22 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   }
 
   const bool batch = p.batch_policy == QF_BATCH_PAPER;
-  const bool resident = p.engine == QF_ENGINE_RESIDENT ||
+  // the batch policy runs resident when this call is the whole batch and all
+  // of its starts fit on the GPU at once (one CTA each, grid barrier per sweep)
+  bool resident_batch = false;
+  if (batch && p.batch_reduce == nullptr && p.engine == QF_ENGINE_AUTO &&
+      c.n <= kResidentMaxQubits && c.p <= kResMaxGates && p.max_iters > 0 &&
+      resident_batch_default()) {
+    int maxm = 1;
+    for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
+    const auto kern = resident_kernel(c.n, maxm);
+    const size_t smem = (size_t)N * N * 16 + 8 * 64 * 16;
+    int per_sm = 0;
+    QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, resident_threads(c.n), smem));
+    resident_batch = (long long)S <= (long long)per_sm * E.nsm;
+  }
+  const bool resident = p.engine == QF_ENGINE_RESIDENT || resident_batch ||
                         (p.engine == QF_ENGINE_AUTO && !batch && c.n <= kResidentMaxQubits &&
                          c.p <= kResMaxGates);
   int last = 0;  // last sweep enqueued (streaming engine)
@@ -1056,18 +1087,27 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     const size_t smem = (size_t)N * N * 16 + 8 * 64 * 16;
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
-    const bool small = c.n <= 4;
-    auto kern = small ? (maxm == 1 ? k_resident<2, false, true> : maxm == 2 ? k_resident<4, false, true>
-                                                                           : k_resident<8, false, true>)
-                      : (maxm == 1 ? k_resident<2, false> : maxm == 2 ? k_resident<4, false>
-                                                                     : k_resident<8, false>);
+    auto kern = resident_kernel(c.n, maxm);
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
     if (const char *e = getenv("QF_RES_CTAS")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
-    const int g = std::max(1, std::min(S, std::max(1, per_sm) * E.nsm));
+    int g = std::max(1, std::min(S, std::max(1, per_sm) * E.nsm));
+    if (resident_batch) {  // one CTA per start, all resident; per-sweep counts
+      g = S;
+      A.batch = 1;
+      A.bcnt = reinterpret_cast<unsigned *>(W + E.L.bcnt);
+      A.gbar = A.bcnt + 3 * ((size_t)p.max_iters + 1);
+      QF_CHECK(cudaMemsetAsync(A.bcnt, 0, (3 * ((size_t)p.max_iters + 1) + 2) * sizeof(unsigned), st));
+    }
     const int slot = E.prof.on ? E.prof.open(2, st) : -1;
-    kern<<<g, threads, smem, st>>>(A);
+    if (resident_batch) {  // co-scheduling guaranteed (or an error, never a hang)
+      void *args[] = {&A};
+      QF_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(g),
+                                           dim3(threads), args, smem, st));
+    } else {
+      kern<<<g, threads, smem, st>>>(A);
+    }
     if (slot >= 0) E.prof.close(slot, st);
     E.launches++;
     QF_CHECK(cudaGetLastError());

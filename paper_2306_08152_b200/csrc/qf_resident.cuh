@@ -68,6 +68,12 @@ struct ResidentArgs {
   int nprob;
   int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
+  // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
+  // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
+  // bcnt[3 * it + {0: converged, 1: running and not yet plateaued, 2: running}]
+  int batch;
+  unsigned *bcnt;
+  unsigned *gbar;  // [0] arrivals (monotone), [1] released generation
   double dist_tol, diff_tol_a, diff_tol_r, long_diff_r, beta;
   int long_diff_count, min_iters, max_iters, reset_iters, ring;
   double *hist;
@@ -410,6 +416,25 @@ __device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
 
 // rest-index bits (of gate g) that belong to the location `next_mask`
 
+// Grid-wide barrier for a launch whose CTAs are all resident (checked by the
+// host against the occupancy before choosing this path): arrivals count up
+// monotonically, the last arriver of generation g releases it.
+__device__ __forceinline__ void res_grid_barrier(unsigned *gbar, unsigned nblocks, unsigned &gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned arrived = atomicAdd(&gbar[0], 1u) + 1u;
+    if (arrived == nblocks * (gen + 1u)) {
+      atomicExch(&gbar[1], gen + 1u);
+    } else {
+      while (atomicAdd(&gbar[1], 0u) < gen + 1u) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  gen++;
+  __syncthreads();
+}
+
 // Schedule of one TwoSidedSweep as 2p steps: j < p -> (gate p-1-j, backward),
 // j >= p -> (gate j-p, forward).  Step j's operands live in buffer j & 1.
 // (Overlapping the next gate's polar factor with this sandwich on the other
@@ -437,8 +462,11 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
   const int sw0 = 0;
   const bool serial = tid >= sw0 && tid < sw0 + 32;
   const int lane = tid - sw0;
-  for (;;) {
-    if (tid == 0) s_start = atomicAdd(A.counter, 1);
+  __shared__ int s_plat, s_fail, s_bstop;
+  unsigned gen = 0;
+  for (int pass = 0;; pass++) {
+    if (tid == 0) s_start = A.batch ? (pass == 0 ? (int)blockIdx.x : A.S) : atomicAdd(A.counter, 1);
+    if (tid == 0) s_plat = s_fail = s_bstop = 0;
     __syncthreads();
     const int s = s_start;
     if (s >= A.S) break;
@@ -590,10 +618,27 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
               if (v == 0 && it >= A.max_iters) v = 4;
             }
           }
-          s_verdict = v;
+          if (A.batch && it > 0) {
+            // the batch decides (reading R22): plateaus do not
+            // stop a start; a failed start stops counting (it keeps sweeping
+            // NaNs until the batch ends, its verdict fixed)
+            if (v == 5 || s_fail) {
+              s_fail = 1;
+              v = 5;
+            } else {
+              if ((v == 2 || v == 3) && s_plat == 0) s_plat = v;
+              unsigned *cnt = A.bcnt + 3LL * it;
+              atomicAdd(&cnt[2], 1u);
+              if (v == 1) atomicAdd(&cnt[0], 1u);
+              else if (s_plat == 0) atomicAdd(&cnt[1], 1u);
+            }
+            s_verdict = v;  // provisional; replaced after the barrier
+          } else {
+            s_verdict = v;
+          }
           A.delta[s] = c;
           A.iters[s] = it;
-          A.verdict[s] = v;
+          if (!(A.batch && it > 0)) A.verdict[s] = v;
         }
         if (A.R > 0 && it >= 1 && it <= A.R) {
           const int slot = A.rec_slot[s];
@@ -606,7 +651,26 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
         }
       }
       __syncthreads();
-      if (s_verdict != 0) break;
+      if (A.batch && it > 0) {
+        res_grid_barrier(A.gbar, gridDim.x, gen);
+        if (tid == 0) {
+          const unsigned *cnt = A.bcnt + 3LL * it;
+          const unsigned c0 = atomicAdd(const_cast<unsigned *>(&cnt[0]), 0u);
+          const unsigned c1 = atomicAdd(const_cast<unsigned *>(&cnt[1]), 0u);
+          const bool any_conv = c0 > 0;
+          const bool stop = any_conv || c1 == 0 || it >= A.max_iters;
+          int v = s_verdict;
+          if (stop) {
+            if (!s_fail) v = v == 1 ? 1 : (s_plat ? s_plat : (any_conv ? 6 : 4));
+            A.verdict[s] = v;
+          }
+          s_bstop = stop ? 1 : 0;
+        }
+        __syncthreads();
+        if (s_bstop) break;
+      } else if (s_verdict != 0) {
+        break;
+      }
       if (it % A.reset_iters == 0) res_init<MAXD>(A, V, ct, gdesc, s, Lb);
       prepare(0, false);  // operands of the next sweep's first step
     }

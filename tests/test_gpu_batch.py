@@ -1,5 +1,6 @@
 """NEXT-1 on the GPU: the batch termination policy (reading R22)
-of the streaming engine against the batch oracle (tests/test_batch_policy.py
+(resident engine for co-resident batches, streaming otherwise) against the
+batch oracle (tests/test_batch_policy.py
 pins the oracle side), on the same seeded inputs: every start's verdict and
 sweep count agree and the final Delta within the north_star 1e-10.  The
 cross-process reduction is exercised through qf_params.batch_reduce with a
@@ -125,3 +126,27 @@ def test_batch_reduce_failure_is_reported():
         qf.qf_instantiate(qf.Circuit(n, locs, kinds, cm), V, init,
                           batch_policy=qf.QF_BATCH_PAPER, batch_reduce=cb, max_iters=10)
     assert e.value.status == qf.QF_E_NCCL
+
+
+def test_batch_resident_matches_streaming():
+    """The co-resident batch (one CTA per start, grid barrier per sweep) and
+    the streaming batch (host decision per sweep) give the same verdicts and
+    sweep counts, Delta within 1e-10."""
+    import os
+
+    w = qfgen.workload("C3+")
+    c = qf.Circuit(w.n, w.locs, w.kinds, w.const_mats)
+    V, init = w.target_unitary(), w.initial(0, 256)
+    a = qf.qf_instantiate(c, V, init, batch_policy=qf.QF_BATCH_PAPER, max_iters=w.max_iters)
+    old = os.environ.get("QF_RES_BATCH")
+    os.environ["QF_RES_BATCH"] = "0"
+    try:
+        b = qf.qf_instantiate(c, V, init, batch_policy=qf.QF_BATCH_PAPER, max_iters=w.max_iters)
+    finally:
+        if old is None:
+            del os.environ["QF_RES_BATCH"]
+        else:
+            os.environ["QF_RES_BATCH"] = old
+    assert a.stats["engine"] == qf.QF_ENGINE_RESIDENT and b.stats["engine"] == qf.QF_ENGINE_STREAM
+    assert np.array_equal(a.verdict, b.verdict) and np.array_equal(a.iters, b.iters)
+    assert np.abs(a.delta - b.delta).max() < TOL
