@@ -84,7 +84,11 @@ typedef enum {
  *     at max_iters.  Verdicts then: CONVERGED for converged starts, the
  *     first plateau kind for plateaued ones, BATCH_STOPPED (stop on another
  *     start's convergence) or MAX_ITER for the rest; NUMERIC_FAIL starts
- *     stop on their own and do not hold the batch.  Streaming engine only.
+ *     stop on their own and do not hold the batch.  A call that is the
+ *     whole batch (batch_reduce NULL) and fits on the GPU at once (n <= 6)
+ *     runs resident in one cooperative launch with a grid barrier per
+ *     sweep; otherwise the streaming engine decides on the host after each
+ *     sweep.  QF_ENGINE_RESIDENT with this policy is rejected (QF_E_ARG).
  * With several processes (one shard of the batch each), the per-sweep
  * counts are summed over the batch by a caller-supplied reduction. */
 typedef enum { QF_BATCH_PER_START = 0, QF_BATCH_PAPER = 1 } qf_batch_policy;
