@@ -814,6 +814,26 @@ struct Engine {
 
   int *sweep_index() const { return reinterpret_cast<int *>(ws + L.counters) + 8; }
 
+  // algorithmic bytes and launch counts of the contexts 0..last (launches of
+  // context j moved their bytes for the h_nact[j] starts active then),
+  // accumulated across waves; the per-context counters restart at zero
+  double acc_sw_b = 0.0, acc_env_b = 0.0, acc_trace_b = 0.0;
+  long long acc_sw_n = 0, acc_env_n = 0;
+  void account(int last, const int *h_nact) {
+    const double ct_bytes = 32.0 * (double)N * (double)N;
+    for (int j = 0; j <= last && j < (int)sw_ctx.size(); j++) {
+      const double na = (double)h_nact[j];
+      acc_sw_b += na * ct_bytes * (double)sw_ctx[j];
+      acc_env_b += na * (double)env_bytes_ctx[j];
+      acc_sw_n += sw_ctx[j];
+      acc_env_n += env_ctx[j];
+      if (j < last) acc_trace_b += na * 16.0 * N;
+    }
+    std::fill(sw_ctx.begin(), sw_ctx.end(), 0);
+    std::fill(env_ctx.begin(), env_ctx.end(), 0);
+    std::fill(env_bytes_ctx.begin(), env_bytes_ctx.end(), 0);
+  }
+
   cudaError_t trace(int it, const int *it_dev = nullptr) {
     TraceArgs A{};
     A.it_dev = it_dev;
@@ -862,6 +882,16 @@ struct Engine {
 };
 
 }  // namespace
+
+// starts per L2-resident wave of the streaming engine (see engine_run)
+int wave_size(int S, long long ct_bytes) {
+  if (const char *e = getenv("QF_WAVE")) {
+    const int w = atoi(e);
+    return w <= 0 ? S : std::min(S, w);
+  }
+  return S;  // default one wave: 96-start L2 waves measured 1.75x slower on C5
+             // (small passes leave the GPU launch- and latency-bound)
+}
 
 // the single-problem resident kernel for n qubits and largest arity maxm
 using ResidentKernel = void (*)(ResidentArgs);
@@ -1112,9 +1142,15 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     E.launches++;
     QF_CHECK(cudaGetLastError());
   } else {
-  // ---- a2: InitCircuitTensor
+  // ---- a2: InitCircuitTensor (per wave below on the per-start path)
   E.ctx = 0;
-  QF_CHECK(E.init_ct());
+  // L2-resident waves (per-start policy): when all tensors exceed the L2,
+  // starts run to their verdicts in waves whose tensors fit in it, so every
+  // pass of a wave streams through L2 instead of HBM (QF_WAVE=k overrides,
+  // QF_WAVE=0 disables)
+  int wave = S;
+  if (!batch && p.max_iters > 0) wave = wave_size(S, (long long)N * N * 16);
+  if (wave >= S || batch || p.max_iters == 0) QF_CHECK(E.init_ct());
 
   // ---- a3..a7: sweeps until every start has a verdict
   // ---- one sweep's launches (a3..a7); replayed from a CUDA graph after the
@@ -1223,21 +1259,39 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       if (p.reset_iters > 0 && it % p.reset_iters == 0) QF_CHECK(E.init_ct());
     }
   } else {
-    for (int it = 1; it <= p.max_iters; it++) {
-      E.ctx = it - 1;  // this sweep runs on the starts active after sweep it-1
-      QF_CHECK(run_sweep(it));
-      E.ctx = it;
-      if (p.reset_iters > 0 && it % p.reset_iters == 0 && it < p.max_iters) QF_CHECK(E.init_ct());
-      QF_CHECK(cudaMemcpyAsync(&h_nact[it], E.n_active(), sizeof(int), cudaMemcpyDeviceToHost, st));
-      QF_CHECK(cudaEventRecord(ev[it & 1], st));
-      d2h += 4;
-      last = it;
-      // lagged check: the GPU keeps one sweep queued while the host waits
-      if (it >= 2) {
-        QF_CHECK(cudaEventSynchronize(ev[(it - 1) & 1]));
-        if (h_nact[it - 1] == 0) break;
+    for (int w0 = 0; w0 < S; w0 += wave) {
+      const int cnt = std::min(wave, S - w0);
+      if (wave < S) {  // this wave's starts become the active list
+        k_wave_active<<<std::max(1, std::min((cnt + 255) / 256, E.nsm * 4)), 256, 0, st>>>(
+            E.active(), E.n_active(), w0, cnt);
+        E.launches++;
+        QF_CHECK(cudaGetLastError());
+        QF_CHECK(cudaMemsetAsync(it_dev, 0, sizeof(int), st));
+        E.ctx = 0;
+        h_nact[0] = cnt;
+        QF_CHECK(E.init_ct());
       }
-      if (it == p.max_iters) break;
+      last = 0;
+      for (int it = 1; it <= p.max_iters; it++) {
+        E.ctx = it - 1;  // this sweep runs on the starts active after sweep it-1
+        QF_CHECK(run_sweep(it));
+        E.ctx = it;
+        if (p.reset_iters > 0 && it % p.reset_iters == 0 && it < p.max_iters) QF_CHECK(E.init_ct());
+        QF_CHECK(cudaMemcpyAsync(&h_nact[it], E.n_active(), sizeof(int), cudaMemcpyDeviceToHost, st));
+        QF_CHECK(cudaEventRecord(ev[it & 1], st));
+        d2h += 4;
+        last = it;
+        // lagged check: the GPU keeps one sweep queued while the host waits
+        if (it >= 2) {
+          QF_CHECK(cudaEventSynchronize(ev[(it - 1) & 1]));
+          if (h_nact[it - 1] == 0) break;
+        }
+        if (it == p.max_iters) break;
+      }
+      if (wave < S) {  // fold this wave's launch and byte counts into the totals
+        QF_CHECK(cudaStreamSynchronize(st));
+        E.account(last, h_nact);
+      }
     }
   }
   }  // streaming engine
@@ -1302,17 +1356,9 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     }
     // algorithmic bytes: launches of context j moved their bytes for the
     // n_active(j) starts active then
-    const double ct_bytes = 32.0 * (double)N * (double)N;
-    double sw_b = 0.0, env_b = 0.0, trace_b = 0.0;
-    long long sw_n = 0, env_n = 0;
-    for (int j = 0; j <= last && j < (int)E.sw_ctx.size(); j++) {
-      const double na = (double)h_nact[j];
-      sw_b += na * ct_bytes * (double)E.sw_ctx[j];
-      env_b += na * (double)E.env_bytes_ctx[j];
-      sw_n += E.sw_ctx[j];
-      env_n += E.env_ctx[j];
-      if (j < last) trace_b += na * 16.0 * N;
-    }
+    E.account(last, h_nact);  // the single (or last) wave
+    const double sw_b = E.acc_sw_b, env_b = E.acc_env_b, trace_b = E.acc_trace_b;
+    const long long sw_n = E.acc_sw_n, env_n = E.acc_env_n;
     E.prof.drain();
     r.stats.alg_bytes_total = sw_b + env_b + trace_b + (double)S * 16.0 * N * N;  // + V^dagger copy
     r.stats.sandwich_bytes = sw_b;

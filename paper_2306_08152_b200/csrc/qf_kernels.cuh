@@ -915,6 +915,13 @@ __global__ void __launch_bounds__(32 * kTraceWarps) k_trace_mask(const TraceArgs
   }
 }
 
+// active list <- [w0, w0 + cnt) (one L2-resident wave of starts)
+__global__ void k_wave_active(int *active, int *n_active, int w0, int cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    active[i] = w0 + i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_active = cnt;
+}
+
 // sweep index for graph replays of a sweep (read by k_trace_mask)
 __global__ void k_next_sweep(int *it) { *it += 1; }
 
