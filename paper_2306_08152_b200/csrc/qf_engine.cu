@@ -490,9 +490,13 @@ struct Engine {
     A.RT = rt.first;
     A.tiles_per_start = rt.second;
     A.dmma = rows_dmma;
+    // FP64-MMA path: pad rows by one complex so that the 8 rows an mma
+    // fragment touches start on 8 different bank groups (QF_ROWS_PAD=0: off)
+    A.pitch = N + (D == 8 && A.dmma && rows_pad ? 1 : 0);
     const size_t tile_bytes = (size_t)A.RT * D * N * 16;
     A.stages = (int)std::max<size_t>(2, std::min<size_t>(4, (rows_smem_kb * 1024) / tile_bytes));
-    const size_t smem = A.stages * tile_bytes + 2 * D * D * 16 + 2 * A.stages * 8 + 2 * kMaxTileRows * 4 + 16 * 4;
+    const size_t smem = A.stages * ((size_t)A.RT * D * A.pitch * 16) + 2 * D * D * 16 + 2 * A.stages * 8 +
+                        2 * kMaxTileRows * 4 + 16 * 4;
     {
       // bank spreading of phase 2: the gate's bits among basis positions
       // {0,1,2} (g of them, local index bits gl[]) are driven by the upper g
@@ -584,6 +588,7 @@ struct Engine {
   int rows_dmma = getenv("QF_ROWS_DMMA") ? atoi(getenv("QF_ROWS_DMMA")) : 1;
   int rows_smem_kb = getenv("QF_ROWS_SMEM_KB") ? atoi(getenv("QF_ROWS_SMEM_KB")) : 96;
   int rows_minb = getenv("QF_ROWS_MINB") ? atoi(getenv("QF_ROWS_MINB")) : 2;
+  int rows_pad = getenv("QF_ROWS_PAD") ? atoi(getenv("QF_ROWS_PAD")) : 1;
   int reg_grid[4] = {0, 0, 0, 0};
 
   cudaError_t sandwich(const SandwichArgs &A) {

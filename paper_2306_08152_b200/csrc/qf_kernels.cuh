@@ -995,6 +995,8 @@ struct RowTileArgs {
   long long rstride;
   int rdag;
   int RT;               // row-rests per tile
+  int pitch;            // shared-memory row pitch in complex (N, or N + 1 on the
+                        // FP64-MMA path: rows then start on rotating banks)
   int tiles_per_start;  // (N/d)/RT
   int dmma;             // d = 8: left multiply on the FP64 tensor path (mma.m8n8k4)
   int stages;           // ring depth
@@ -1029,10 +1031,10 @@ constexpr int kMaxTileRows = 64;
 template <int D, int MINB = 2>
 __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const RowTileArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  const int N = A.N;
+  const int N = A.N, P = A.pitch;
   const int rows = A.RT * D;
-  const int tile_elems = rows * N;
-  const uint32_t tile_bytes = (uint32_t)tile_elems * 16u;
+  const int tile_elems = rows * P;                      // shared-memory footprint
+  const uint32_t tile_bytes = (uint32_t)(rows * N) * 16u;  // bytes moved per tile
   double2 *tiles = reinterpret_cast<double2 *>(smraw);
   double2 *Ls = tiles + (size_t)A.stages * tile_elems;
   double2 *Rs = Ls + D * D;
@@ -1091,7 +1093,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         if (lane < rows) {
           const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
           ptx::bulk_s2g(A.ct + (long long)s * A.ct_stride + (long long)row * N,
-                        tiles + (size_t)st * tile_elems + (size_t)lane * N, row_bytes);
+                        tiles + (size_t)st * tile_elems + (size_t)lane * P, row_bytes);
           ptx::bulk_commit();
           ptx::bulk_wait_read<0>();
         }
@@ -1104,7 +1106,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         __syncwarp();
         if (lane < rows) {
           const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
-          ptx::bulk_g2s(tiles + (size_t)st * tile_elems + (size_t)lane * N,
+          ptx::bulk_g2s(tiles + (size_t)st * tile_elems + (size_t)lane * P,
                         A.ct + (long long)s * A.ct_stride + (long long)row * N, row_bytes,
                         &full[st]);
         }
@@ -1167,34 +1169,34 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         const int chunks = A.RT * (N >> 3);
         for (int ch = warp; ch < chunks; ch += kRowThreads / 32) {
           const int rl = ch / (N >> 3), col0 = (ch - rl * (N >> 3)) << 3;
-          double2 *base = tile + (size_t)rl * 8 * N + col0;
+          double2 *base = tile + (size_t)rl * 8 * P + col0;
           double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
 #pragma unroll
           for (int kb = 0; kb < 2; kb++) {
-            const double2 x = base[(kb * 4 + fk) * N + fr];  // B[k = kb*4 + fk][n = fr]
+            const double2 x = base[(kb * 4 + fk) * P + fr];  // B[k = kb*4 + fk][n = fr]
             ptx::dmma(cr0, cr1, lr[kb], x.x);
             ptx::dmma(cr0, cr1, nli[kb], x.y);
             ptx::dmma(ci0, ci1, lr[kb], x.y);
             ptx::dmma(ci0, ci1, li[kb], x.x);
           }
           __syncwarp();  // every lane has read its X before Y overwrites it
-          base[fr * N + 2 * fk] = make_double2(cr0, ci0);  // C[m = fr][n = 2 fk + {0, 1}]
-          base[fr * N + 2 * fk + 1] = make_double2(cr1, ci1);
+          base[fr * P + 2 * fk] = make_double2(cr0, ci0);  // C[m = fr][n = 2 fk + {0, 1}]
+          base[fr * P + 2 * fk + 1] = make_double2(cr1, ci1);
         }
       }
     }
     for (int it = tid; it < (D == 8 && A.dmma ? 0 : A.RT * N); it += kRowThreads) {
       const int rl = it / N, col = it - rl * N;
-      double2 *base = tile + (size_t)rl * D * N + col;
+      double2 *base = tile + (size_t)rl * D * P + col;
       double2 x[D];
 #pragma unroll
-      for (int a = 0; a < D; a++) x[a] = base[a * N];
+      for (int a = 0; a < D; a++) x[a] = base[a * P];
 #pragma unroll
       for (int a = 0; a < D; a++) {
         double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k], acc);
-        base[a * N] = acc;
+        base[a * P] = acc;
       }
     }
 #ifdef QF_POLAR_COUNT
@@ -1204,9 +1206,11 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
       csync();
       if constexpr (D == 8) {
         if (A.dmma) {
-          // phase 2 on the tensor path: 8 items (rows of the mma) x 8 local
-          // columns; R in registers (B[k][n] = R[k][n]); each lane gathers
-          // its item's columns ins(k, c) and writes the item's outputs
+          // phase 2 on the tensor path: the 8 items of an mma (its rows m)
+          // are the 8 tile rows a of one row group at one column rest c, so
+          // with the padded pitch their accesses start on 8 different bank
+          // groups whatever basis bits the gate owns; R in registers
+          // (B[k][n] = R[k][n]); each lane gathers its item's columns ins(k, c)
           const int lane = tid & 31, warp = tid >> 5;
           const int fr = lane >> 2, fk = lane & 3;
           double rr[2], ri[2], nri[2];
@@ -1217,12 +1221,10 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
             ri[kb] = r.y;
             nri[kb] = -r.y;
           }
-          const int groups = (A.RT * N) >> 3;
+          const int groups = A.RT * NC;
           for (int gi = warp; gi < groups; gi += kRowThreads / 32) {
-            const int it = (gi << 3) + fr;
-            const int rl = it / N, rem = it - rl * N;
-            const int a = rem / NC, c = rem - a * NC;
-            double2 *row = tile + (size_t)(rl * D + a) * N;
+            const int rl = gi / NC, c = gi - rl * NC;
+            double2 *row = tile + (size_t)(rl * D + fr) * P;
             const int cb = spread_rest(A.b, c);
             double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
 #pragma unroll
@@ -1244,7 +1246,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
       for (int it = tid; it < (D == 8 && A.dmma ? 0 : A.RT * N); it += kRowThreads) {
         const int rl = it / N, rem = it - rl * N;
         const int a = rem / NC, c = rem - a * NC;
-        double2 *row = tile + (size_t)(rl * D + a) * N;
+        double2 *row = tile + (size_t)(rl * D + a) * P;
         const int cb = spread_rest(A.b, c);
         const int m = sab[8 + (c & 7)];
         double2 z[D];
@@ -1274,7 +1276,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         for (int q = 0; q < rows; q++) {
           const int i = rid[q];
           if ((i & A.nmask) == ap) {
-            const double2 v = tile[(size_t)q * N + ((i & ~A.nmask) | bp)];
+            const double2 v = tile[(size_t)q * P + ((i & ~A.nmask) | bp)];
             acc.x += v.x;
             acc.y += v.y;
           }
@@ -1285,7 +1287,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
     if (A.nx_trace && tid == 64) {
       double2 acc = make_double2(0.0, 0.0);
       for (int q = 0; q < rows; q++) {
-        const double2 v = tile[(size_t)q * N + rid[q]];
+        const double2 v = tile[(size_t)q * P + rid[q]];
         acc.x += v.x;
         acc.y += v.y;
       }
