@@ -490,13 +490,39 @@ struct Engine {
     A.RT = rt.first;
     A.tiles_per_start = rt.second;
     A.dmma = rows_dmma;
-    // FP64-MMA path: pad rows by one complex so that the 8 rows an mma
-    // fragment touches start on 8 different bank groups (QF_ROWS_PAD=0: off)
-    A.pitch = N + (D == 8 && A.dmma && rows_pad ? 1 : 0);
+    A.pitch = N;
+    for (int t = 0; t < 8; t++) {
+      A.roff[t] = 0;
+      A.cperm[t] = t;
+    }
+    if (D == 8 && A.dmma && rows_pad) {
+      // FP64-MMA blocks: a quarter-warp touches rows {2t + kb} (t < 4) at
+      // the two block columns cperm[2q], cperm[2q + 1].  Pair the columns
+      // on the gate bit with the lowest basis position p0 (bank-group
+      // distance delta = 2^p0 mod 8) and offset the rows so that the 8
+      // accesses fall on 8 bank groups: offsets O with O, O + delta disjoint.
+      A.pitch = N + 8;
+      int i0 = 0, p0 = 1 << 30;
+      for (int i = 0; i < 3; i++) {
+        const int pos = ilog2(A.b.abits[1 << i]);
+        if (pos < p0) {
+          p0 = pos;
+          i0 = i;
+        }
+      }
+      for (int t = 0; t < 8; t++) {
+        const int hi = t >> 1, lo = hi & ((1 << i0) - 1);
+        A.cperm[t] = ((hi - lo) << 1) | ((t & 1) << i0) | lo;
+      }
+      static const int O1[4] = {0, 2, 4, 6}, O2[4] = {0, 1, 4, 5}, O4[4] = {0, 1, 2, 3};
+      const int delta = p0 < 3 ? 1 << p0 : 0;
+      const int *O = delta == 2 ? O2 : delta == 4 ? O4 : O1;
+      for (int t = 0; t < 8; t++) A.roff[t] = O[t >> 1];
+    }
     const size_t tile_bytes = (size_t)A.RT * D * N * 16;
     A.stages = (int)std::max<size_t>(2, std::min<size_t>(4, (rows_smem_kb * 1024) / tile_bytes));
-    const size_t smem = A.stages * ((size_t)A.RT * D * A.pitch * 16) + 2 * D * D * 16 + 2 * A.stages * 8 +
-                        2 * kMaxTileRows * 4 + 16 * 4;
+    const size_t smem = A.stages * ((size_t)A.RT * D * A.pitch + 8) * 16 + 2 * D * D * 16 + 2 * A.stages * 8 +
+                        2 * kMaxTileRows * 4 + 32 * 4;
     {
       // bank spreading of phase 2: the gate's bits among basis positions
       // {0,1,2} (g of them, local index bits gl[]) are driven by the upper g

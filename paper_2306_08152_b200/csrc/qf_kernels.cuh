@@ -995,8 +995,10 @@ struct RowTileArgs {
   long long rstride;
   int rdag;
   int RT;               // row-rests per tile
-  int pitch;            // shared-memory row pitch in complex (N, or N + 1 on the
-                        // FP64-MMA path: rows then start on rotating banks)
+  int pitch;            // shared-memory row pitch in complex (N, or N + 8 on the
+                        // two-sided FP64-MMA path)
+  int roff[8];          // tile row q starts at q * pitch + roff[q & 7]
+  int cperm[8];         // FP64-MMA block column order (see the fused path)
   int tiles_per_start;  // (N/d)/RT
   int dmma;             // d = 8: left multiply on the FP64 tensor path (mma.m8n8k4)
   int stages;           // ring depth
@@ -1033,7 +1035,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
   extern __shared__ __align__(128) unsigned char smraw[];
   const int N = A.N, P = A.pitch;
   const int rows = A.RT * D;
-  const int tile_elems = rows * P;                      // shared-memory footprint
+  const int tile_elems = rows * P + 8;                  // shared-memory footprint
   const uint32_t tile_bytes = (uint32_t)(rows * N) * 16u;  // bytes moved per tile
   double2 *tiles = reinterpret_cast<double2 *>(smraw);
   double2 *Ls = tiles + (size_t)A.stages * tile_elems;
@@ -1041,12 +1043,16 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
   uint64_t *full = reinterpret_cast<uint64_t *>(Rs + D * D);
   uint64_t *computed = full + A.stages;
   int *rid_buf = reinterpret_cast<int *>(computed + A.stages);  // 2 x kMaxTileRows
-  int *sab = rid_buf + 2 * kMaxTileRows;                         // abits[8], rot[8]
+  int *sab = rid_buf + 2 * kMaxTileRows;  // abits[8], rot[8], roff[8], cperm[8]
   const int tid = threadIdx.x;
   if (tid < 8) {
     sab[tid] = A.b.abits[tid];
     sab[8 + tid] = A.rot[tid];
+    sab[16 + tid] = A.roff[tid];
+    sab[24 + tid] = A.cperm[tid];
   }
+  // tile row q lives at rowp(q) (complex units from the tile base)
+  auto rowp = [&](int q) { return q * P + sab[16 + (q & 7)]; };
   const bool has_r = A.rsrc != nullptr;
 
   const int nact = *A.n_active;
@@ -1093,7 +1099,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         if (lane < rows) {
           const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
           ptx::bulk_s2g(A.ct + (long long)s * A.ct_stride + (long long)row * N,
-                        tiles + (size_t)st * tile_elems + (size_t)lane * P, row_bytes);
+                        tiles + (size_t)st * tile_elems + rowp(lane), row_bytes);
           ptx::bulk_commit();
           ptx::bulk_wait_read<0>();
         }
@@ -1106,7 +1112,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         __syncwarp();
         if (lane < rows) {
           const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
-          ptx::bulk_g2s(tiles + (size_t)st * tile_elems + (size_t)lane * P,
+          ptx::bulk_g2s(tiles + (size_t)st * tile_elems + rowp(lane),
                         A.ct + (long long)s * A.ct_stride + (long long)row * N, row_bytes,
                         &full[st]);
         }
@@ -1148,14 +1154,73 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
     const long long tq1 = clock64();
 #endif
     double2 *tile = tiles + (size_t)st * tile_elems;
+    bool fused = false;
+    if constexpr (D == 8) fused = A.dmma && has_r;
+    if constexpr (D == 8) {
+      if (fused) {
+        // Two-sided step on the FP64 tensor path, one 8 x 8 block (the 8 rows
+        // of a row group x the 8 columns ins(., c) of column rest c) per warp
+        // iteration, both multiplies in registers:
+        //   stage 1  Y   = L X        (mma k = tile row 2 fk + kb)
+        //   stage 2  Z^T = R^T Y^T    (mma k = local column cperm[2 fk + kb])
+        // The k orders make stage 1's accumulator fragment (lane: Y[fr][cperm[2fk+s]])
+        // exactly stage 2's B fragment, and stage 2's accumulator
+        // (Z[2fk+s][cperm[fr]]) lands on the two elements the lane loaded:
+        // one shared-memory load and one store per element, in place.  The
+        // per-gate row offsets roff and column order cperm put the 8 lanes
+        // of a quarter-warp on 8 different bank groups unless all the gate's
+        // column bits are >= 3 (then 2-way).
+        const int lane = tid & 31, warp = tid >> 5;
+        const int fr = lane >> 2, fk = lane & 3;
+        const int *roff = sab + 16, *cperm = sab + 24;
+        double lr[2], li[2], nli[2], rr[2], ri[2], nri[2];
+#pragma unroll
+        for (int kb = 0; kb < 2; kb++) {
+          const double2 l = Ls[fr * 8 + 2 * fk + kb];
+          lr[kb] = l.x;
+          li[kb] = l.y;
+          nli[kb] = -l.y;
+          const double2 r = Rs[cperm[2 * fk + kb] * 8 + cperm[fr]];
+          rr[kb] = r.x;
+          ri[kb] = r.y;
+          nri[kb] = -r.y;
+        }
+        const int colL = sab[cperm[fr]];
+        const int o0 = 2 * fk * P + roff[2 * fk], o1 = (2 * fk + 1) * P + roff[2 * fk + 1];
+        const int blocks = A.RT * NC;
+        for (int gi = warp; gi < blocks; gi += kRowThreads / 32) {
+          const int rl = gi / NC, c = gi - rl * NC;
+          double2 *blk = tile + (size_t)rl * 8 * P + (spread_rest(A.b, c) | colL);
+          const double2 x0 = blk[o0], x1 = blk[o1];
+          double yr0 = 0.0, yr1 = 0.0, yi0 = 0.0, yi1 = 0.0;
+          ptx::dmma(yr0, yr1, lr[0], x0.x);
+          ptx::dmma(yr0, yr1, nli[0], x0.y);
+          ptx::dmma(yi0, yi1, lr[0], x0.y);
+          ptx::dmma(yi0, yi1, li[0], x0.x);
+          ptx::dmma(yr0, yr1, lr[1], x1.x);
+          ptx::dmma(yr0, yr1, nli[1], x1.y);
+          ptx::dmma(yi0, yi1, lr[1], x1.y);
+          ptx::dmma(yi0, yi1, li[1], x1.x);
+          double zr0 = 0.0, zr1 = 0.0, zi0 = 0.0, zi1 = 0.0;
+          ptx::dmma(zr0, zr1, rr[0], yr0);
+          ptx::dmma(zr0, zr1, nri[0], yi0);
+          ptx::dmma(zi0, zi1, ri[0], yr0);
+          ptx::dmma(zi0, zi1, rr[0], yi0);
+          ptx::dmma(zr0, zr1, rr[1], yr1);
+          ptx::dmma(zr0, zr1, nri[1], yi1);
+          ptx::dmma(zi0, zi1, ri[1], yr1);
+          ptx::dmma(zi0, zi1, rr[1], yi1);
+          blk[o0] = make_double2(zr0, zi0);
+          blk[o1] = make_double2(zr1, zi1);
+        }
+      }
+    }
     // phase 1: left multiply, one column of one row group per item
     if constexpr (D == 8) {
-      if (A.dmma) {
-        // on the FP64 tensor path: Y = L X per 8-column chunk of a row group
-        // as 8 x mma.m8n8k4.f64 (complex = 4 real products per k-block);
-        // L stays in registers, X and Y move as one 16-byte access per lane
-        // per k-block / output pair -- a quarter of the shared-memory
-        // wavefronts of the FMA form (which is bound by them at d = 8)
+      if (A.dmma && !has_r) {
+        // one-sided (InitCircuitTensor) on the FP64 tensor path: Y = L X per
+        // 8-column chunk of a row group as 8 x mma.m8n8k4.f64 (complex = 4
+        // real products per k-block); L stays in registers
         const int lane = tid & 31, warp = tid >> 5;
         const int fr = lane >> 2, fk = lane & 3;
         double lr[2], li[2], nli[2];
@@ -1173,80 +1238,44 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
           double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
 #pragma unroll
           for (int kb = 0; kb < 2; kb++) {
-            const double2 x = base[(kb * 4 + fk) * P + fr];  // B[k = kb*4 + fk][n = fr]
+            const int q = kb * 4 + fk;
+            const double2 x = base[q * P + sab[16 + q] + fr];  // B[k = kb*4 + fk][n = fr]
             ptx::dmma(cr0, cr1, lr[kb], x.x);
             ptx::dmma(cr0, cr1, nli[kb], x.y);
             ptx::dmma(ci0, ci1, lr[kb], x.y);
             ptx::dmma(ci0, ci1, li[kb], x.x);
           }
           __syncwarp();  // every lane has read its X before Y overwrites it
-          base[fr * P + 2 * fk] = make_double2(cr0, ci0);  // C[m = fr][n = 2 fk + {0, 1}]
-          base[fr * P + 2 * fk + 1] = make_double2(cr1, ci1);
+          double2 *o = base + fr * P + sab[16 + fr];
+          o[2 * fk] = make_double2(cr0, ci0);  // C[m = fr][n = 2 fk + {0, 1}]
+          o[2 * fk + 1] = make_double2(cr1, ci1);
         }
       }
     }
     for (int it = tid; it < (D == 8 && A.dmma ? 0 : A.RT * N); it += kRowThreads) {
       const int rl = it / N, col = it - rl * N;
-      double2 *base = tile + (size_t)rl * D * P + col;
       double2 x[D];
 #pragma unroll
-      for (int a = 0; a < D; a++) x[a] = base[a * P];
+      for (int a = 0; a < D; a++) x[a] = tile[rowp(rl * D + a) + col];
 #pragma unroll
       for (int a = 0; a < D; a++) {
         double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
         for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k], acc);
-        base[a * P] = acc;
+        tile[rowp(rl * D + a) + col] = acc;
       }
     }
 #ifdef QF_POLAR_COUNT
     const long long tq2 = clock64();
 #endif
-    if (has_r) {
+    if (has_r && !fused) {
       csync();
-      if constexpr (D == 8) {
-        if (A.dmma) {
-          // phase 2 on the tensor path: the 8 items of an mma (its rows m)
-          // are the 8 tile rows a of one row group at one column rest c, so
-          // with the padded pitch their accesses start on 8 different bank
-          // groups whatever basis bits the gate owns; R in registers
-          // (B[k][n] = R[k][n]); each lane gathers its item's columns ins(k, c)
-          const int lane = tid & 31, warp = tid >> 5;
-          const int fr = lane >> 2, fk = lane & 3;
-          double rr[2], ri[2], nri[2];
-#pragma unroll
-          for (int kb = 0; kb < 2; kb++) {
-            const double2 r = Rs[(kb * 4 + fk) * 8 + fr];
-            rr[kb] = r.x;
-            ri[kb] = r.y;
-            nri[kb] = -r.y;
-          }
-          const int groups = A.RT * NC;
-          for (int gi = warp; gi < groups; gi += kRowThreads / 32) {
-            const int rl = gi / NC, c = gi - rl * NC;
-            double2 *row = tile + (size_t)(rl * D + fr) * P;
-            const int cb = spread_rest(A.b, c);
-            double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
-#pragma unroll
-            for (int kb = 0; kb < 2; kb++) {
-              const double2 y = row[cb | sab[kb * 4 + fk]];  // A[m = fr][k = kb*4 + fk]
-              ptx::dmma(cr0, cr1, y.x, rr[kb]);
-              ptx::dmma(cr0, cr1, y.y, nri[kb]);
-              ptx::dmma(ci0, ci1, y.x, ri[kb]);
-              ptx::dmma(ci0, ci1, y.y, rr[kb]);
-            }
-            __syncwarp();
-            row[cb | sab[2 * fk]] = make_double2(cr0, ci0);  // C[m = fr][n = 2 fk + {0, 1}]
-            row[cb | sab[2 * fk + 1]] = make_double2(cr1, ci1);
-          }
-        }
-      }
       // phase 2: right multiply, d columns ins(b, c) of one row per item,
       // local column order permuted by m = rot[c & 7] (R's indices follow)
-      for (int it = tid; it < (D == 8 && A.dmma ? 0 : A.RT * N); it += kRowThreads) {
+      for (int it = tid; it < A.RT * N; it += kRowThreads) {
         const int rl = it / N, rem = it - rl * N;
         const int a = rem / NC, c = rem - a * NC;
-        double2 *row = tile + (size_t)(rl * D + a) * P;
+        double2 *row = tile + rowp(rl * D + a);
         const int cb = spread_rest(A.b, c);
         const int m = sab[8 + (c & 7)];
         double2 z[D];
@@ -1276,7 +1305,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         for (int q = 0; q < rows; q++) {
           const int i = rid[q];
           if ((i & A.nmask) == ap) {
-            const double2 v = tile[(size_t)q * P + ((i & ~A.nmask) | bp)];
+            const double2 v = tile[rowp(q) + ((i & ~A.nmask) | bp)];
             acc.x += v.x;
             acc.y += v.y;
           }
@@ -1287,7 +1316,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
     if (A.nx_trace && tid == 64) {
       double2 acc = make_double2(0.0, 0.0);
       for (int q = 0; q < rows; q++) {
-        const double2 v = tile[(size_t)q * P + rid[q]];
+        const double2 v = tile[rowp(q) + rid[q]];
         acc.x += v.x;
         acc.y += v.y;
       }

@@ -27,6 +27,9 @@ for r in rows[2:]:
         if k in h:
             i = h.index(k)
             print(f"{k:70s} {r[i]} {u[i]}")
+    for i in range(len(h)):  # FP64 tensor (DMMA) pipe, when the kernel uses it
+        if "dmma" in h[i] and "pct_of_peak_sustained_active" in h[i] and r[i] not in ("", "n/a"):
+            print(f"{h[i]:70s} {r[i]} {u[i]}")
     st = [(h[i], float(r[i].replace(",", ""))) for i in range(len(h))
           if re.match(r"smsp__pcsamp_warps_issue_stalled_\w+$", h[i]) and r[i] not in ("", "n/a")]
     tot = sum(v for _, v in st) or 1
