@@ -491,6 +491,8 @@ struct Engine {
     A.tiles_per_start = rt.second;
     A.dmma = rows_dmma;
     A.pitch = N;
+    A.ilp2 = rows_ilp2;
+    A.m3 = rows_3m;
     for (int t = 0; t < 8; t++) {
       A.roff[t] = 0;
       A.cperm[t] = t;
@@ -615,6 +617,8 @@ struct Engine {
   int rows_smem_kb = getenv("QF_ROWS_SMEM_KB") ? atoi(getenv("QF_ROWS_SMEM_KB")) : 96;
   int rows_minb = getenv("QF_ROWS_MINB") ? atoi(getenv("QF_ROWS_MINB")) : 2;
   int rows_pad = getenv("QF_ROWS_PAD") ? atoi(getenv("QF_ROWS_PAD")) : 1;
+  int rows_ilp2 = getenv("QF_ROWS_ILP2") ? atoi(getenv("QF_ROWS_ILP2")) : 1;
+  int rows_3m = getenv("QF_ROWS_3M") ? atoi(getenv("QF_ROWS_3M")) : 1;
   int reg_grid[4] = {0, 0, 0, 0};
 
   cudaError_t sandwich(const SandwichArgs &A) {

@@ -999,6 +999,8 @@ struct RowTileArgs {
                         // two-sided FP64-MMA path)
   int roff[8];          // tile row q starts at q * pitch + roff[q & 7]
   int cperm[8];         // FP64-MMA block column order (see the fused path)
+  int ilp2;             // fused path: two blocks per warp iteration
+  int m3;               // fused path: 3M complex products
   int tiles_per_start;  // (N/d)/RT
   int dmma;             // d = 8: left multiply on the FP64 tensor path (mma.m8n8k4)
   int stages;           // ring depth
@@ -1188,10 +1190,8 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         const int colL = sab[cperm[fr]];
         const int o0 = 2 * fk * P + roff[2 * fk], o1 = (2 * fk + 1) * P + roff[2 * fk + 1];
         const int blocks = A.RT * NC;
-        for (int gi = warp; gi < blocks; gi += kRowThreads / 32) {
-          const int rl = gi / NC, c = gi - rl * NC;
-          double2 *blk = tile + (size_t)rl * 8 * P + (spread_rest(A.b, c) | colL);
-          const double2 x0 = blk[o0], x1 = blk[o1];
+        // one block: loads, 8 + 8 dependent MMAs, stores
+        auto block_mma = [&](const double2 x0, const double2 x1, double2 &z0, double2 &z1) {
           double yr0 = 0.0, yr1 = 0.0, yi0 = 0.0, yi1 = 0.0;
           ptx::dmma(yr0, yr1, lr[0], x0.x);
           ptx::dmma(yr0, yr1, nli[0], x0.y);
@@ -1210,8 +1210,77 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
           ptx::dmma(zr0, zr1, nri[1], yi1);
           ptx::dmma(zi0, zi1, ri[1], yr1);
           ptx::dmma(zi0, zi1, rr[1], yi1);
-          blk[o0] = make_double2(zr0, zi0);
-          blk[o1] = make_double2(zr1, zi1);
+          z0 = make_double2(zr0, zi0);
+          z1 = make_double2(zr1, zi1);
+        };
+        // 3M form (QF_ROWS_3M=1): three real products per complex k-block,
+        //   T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi),
+        //   re = T1 - T2, im = T3 - T1 - T2
+        double ls[2], rs[2];
+#pragma unroll
+        for (int kb = 0; kb < 2; kb++) {
+          ls[kb] = lr[kb] + li[kb];
+          rs[kb] = rr[kb] + ri[kb];
+        }
+        auto block_3m = [&](const double2 x0, const double2 x1, double2 &z0, double2 &z1) {
+          double a1 = 0.0, b1 = 0.0, a2 = 0.0, b2 = 0.0, a3 = 0.0, b3 = 0.0;
+          ptx::dmma(a1, b1, lr[0], x0.x);
+          ptx::dmma(a2, b2, li[0], x0.y);
+          ptx::dmma(a3, b3, ls[0], x0.x + x0.y);
+          ptx::dmma(a1, b1, lr[1], x1.x);
+          ptx::dmma(a2, b2, li[1], x1.y);
+          ptx::dmma(a3, b3, ls[1], x1.x + x1.y);
+          const double yr0 = a1 - a2, yr1 = b1 - b2;
+          const double yi0 = a3 - a1 - a2, yi1 = b3 - b1 - b2;
+          double c1 = 0.0, d1 = 0.0, c2 = 0.0, d2 = 0.0, c3 = 0.0, d3 = 0.0;
+          ptx::dmma(c1, d1, rr[0], yr0);
+          ptx::dmma(c2, d2, ri[0], yi0);
+          ptx::dmma(c3, d3, rs[0], yr0 + yi0);
+          ptx::dmma(c1, d1, rr[1], yr1);
+          ptx::dmma(c2, d2, ri[1], yi1);
+          ptx::dmma(c3, d3, rs[1], yr1 + yi1);
+          z0 = make_double2(c1 - c2, c3 - c1 - c2);
+          z1 = make_double2(d1 - d2, d3 - d1 - d2);
+        };
+        auto block_ptr = [&](int gi) {
+          const int rl = gi / NC, c = gi - rl * NC;
+          return tile + (size_t)rl * 8 * P + (spread_rest(A.b, c) | colL);
+        };
+        if (A.ilp2) {
+          // two blocks per iteration: two independent MMA chains in flight
+          // (the second is a duplicate of the first, not stored, on the tail)
+          constexpr int W = kRowThreads / 32;
+          for (int gi = warp; gi < blocks; gi += 2 * W) {
+            const bool two = gi + W < blocks;  // warp-uniform
+            double2 *ba = block_ptr(gi), *bb = block_ptr(two ? gi + W : gi);
+            const double2 xa0 = ba[o0], xa1 = ba[o1], xb0 = bb[o0], xb1 = bb[o1];
+            double2 za0, za1, zb0, zb1;
+            if (A.m3) {
+              block_3m(xa0, xa1, za0, za1);
+              block_3m(xb0, xb1, zb0, zb1);
+            } else {
+              block_mma(xa0, xa1, za0, za1);
+              block_mma(xb0, xb1, zb0, zb1);
+            }
+            ba[o0] = za0;
+            ba[o1] = za1;
+            if (two) {
+              bb[o0] = zb0;
+              bb[o1] = zb1;
+            }
+          }
+        } else {
+          for (int gi = warp; gi < blocks; gi += kRowThreads / 32) {
+            double2 *blk = block_ptr(gi);
+            const double2 x0 = blk[o0], x1 = blk[o1];
+            double2 z0, z1;
+            if (A.m3)
+              block_3m(x0, x1, z0, z1);
+            else
+              block_mma(x0, x1, z0, z1);
+            blk[o0] = z0;
+            blk[o1] = z1;
+          }
         }
       }
     }
