@@ -553,6 +553,17 @@ struct Engine {
       part_dir = next_dir;
       part_tiles = A.tiles_per_start;
     }
+    else if (grp_next_w > 0 && A.tiles_per_start <= L.max_parts) {
+      // grouped steps: T of the next group (its W as a pseudo-gate)
+      const Bits nb = make_bits_loc(c.n, grp_next_wq, grp_next_w);
+      A.nx_env = 1;
+      A.nd = nb.d;
+      A.nmask = nb.abits[nb.d - 1];
+      for (int a = 0; a < nb.d; a++) A.nab[a] = nb.abits[a];
+      A.part = reinterpret_cast<double2 *>(ws + L.part);
+      A.part_stride = (long long)L.max_parts * 64;
+      grp_part_tiles = A.tiles_per_start;
+    }
     if (next_trace) {
       A.nx_trace = 1;
       A.tpart = reinterpret_cast<double2 *>(ws + L.tpart);
@@ -580,6 +591,12 @@ struct Engine {
 
   // next step of the schedule whose inputs the row-tile epilogue produces
   int next_k = -1, next_dir = 0;
+  // grouped steps: W of the next group (the flush epilogue's pseudo-gate) and
+  // the tiles of the partials it left (0 = none: the next group gathers)
+  int grp_next_w = 0, grp_next_wq[3] = {0, 0, 0}, grp_part_tiles = 0;
+  // measured 5.6 % slower at C5 (3 sweeps 3917 -> 4137 ms, same box): the
+  // 64-entry epilogue on every flush tile costs more than the gather it saves
+  int group_fuse = getenv("QF_GROUP_FUSE") ? atoi(getenv("QF_GROUP_FUSE")) : 0;
   bool next_trace = false;
   // fused partials available for env(part_k, part_dir) / the trace
   int part_k = -1, part_dir = 0, part_tiles = 0, tpart_tiles = 0;
@@ -753,9 +770,16 @@ struct Engine {
 
   // NEXT-3: one group of steps (see k_group): T gather + every update in one
   // warp-per-start launch, then one sandwich pass with the accumulated (Lp, Rp)
-  cudaError_t group_steps(const StepGroup &G) {
+  cudaError_t group_steps(const StepGroup &G, const StepGroup *next) {
     const int w = (int)G.wq.size();
     GroupArgs A{};
+    const int ptiles = grp_part_tiles;
+    grp_part_tiles = 0;
+    if (ptiles > 0) {
+      A.part = reinterpret_cast<const double2 *>(ws + L.part);
+      A.part_stride = (long long)L.max_parts * 64;
+      A.part_tiles = ptiles;
+    }
     A.bw = make_bits_loc(c.n, G.wq.data(), w);
     A.N = N;
     A.ct = ct();
@@ -796,7 +820,8 @@ struct Engine {
     if (slot >= 0) prof.close(slot, st);
     launches++;
     env_ctx[ctx]++;
-    env_bytes_ctx[ctx] += (long long)16 * N * (1 << w) + 64LL * 16 * A.nsteps;
+    env_bytes_ctx[ctx] += (ptiles > 0 ? 16LL * ptiles * (1 << (2 * w)) : (long long)16 * N * (1 << w)) +
+                          64LL * 16 * A.nsteps;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     SandwichArgs B{};
@@ -813,7 +838,14 @@ struct Engine {
     B.rdag = 0;
     next_k = -1;
     next_trace = false;
-    return sandwich(B);
+    grp_next_w = 0;
+    if (next && group_fuse) {
+      grp_next_w = (int)next->wq.size();
+      for (int i = 0; i < grp_next_w; i++) grp_next_wq[i] = next->wq[i];
+    }
+    const cudaError_t es = sandwich(B);
+    grp_next_w = 0;
+    return es;
   }
 
   // InitCircuitTensor for the active starts
@@ -1204,8 +1236,9 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     if (batch && (e = cudaMemsetAsync(E.batch_counts(), 0, 3 * sizeof(unsigned), E.st)) != cudaSuccess)
       return e;
     if (!groups.empty()) {
-      for (const auto &G : groups)
-        if ((e = E.group_steps(G)) != cudaSuccess) return e;
+      for (size_t i = 0; i < groups.size(); i++)
+        if ((e = E.group_steps(groups[i], i + 1 < groups.size() ? &groups[i + 1] : nullptr)) != cudaSuccess)
+          return e;
     } else {
       for (int k = c.p - 1; k >= 0; k--)
         if ((e = E.step(k, 0)) != cudaSuccess) return e;

@@ -1529,6 +1529,11 @@ struct GroupArgs {
   int polar_jacobi;
   double2 *ops;  // per start: Lp [64], Rp [64]
   long long ops_stride;
+  // T from the previous group's flush epilogue (row-tile partials on W, tile
+  // order) instead of the strided gather; nullptr = gather
+  const double2 *part;
+  long long part_stride;
+  int part_tiles;
   int nsteps;
   GroupStep st[kGroupMax];
 };
@@ -1567,6 +1572,19 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
   constexpr int OPL = DD >= 32 ? DD / 32 : 1;
   for (int ai = blockIdx.x * kEnvWarps + w; ai < nact; ai += gridDim.x * kEnvWarps) {
     const int s = A.active[ai];
+    if (A.part) {
+      // T = sum over the flushing sandwich's tiles, tile order
+      const double2 *pp = A.part + (long long)s * A.part_stride;
+      for (int o = lane; o < DD; o += 32) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int t = 0; t < A.part_tiles; t++) {
+          const double2 v = pp[t * DD + o];
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        T[o] = acc;
+      }
+    } else {
     // T = PT_{not W}(ct), rests ascending per lane, fixed xor tree
     const double2 *cts = A.ct + (long long)s * A.ct_stride;
     const int k = lane % SPLIT;
@@ -1587,6 +1605,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
       }
       if (k == 0) T[o] = acc;
+    }
     }
     for (int o = lane; o < DD; o += 32) {
       const double2 one = make_double2(o / DW == o % DW ? 1.0 : 0.0, 0.0);
