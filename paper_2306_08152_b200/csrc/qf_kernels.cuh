@@ -701,6 +701,49 @@ __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
   }
 }
 
+// P[a][b] = sum_r ct[ins(a, r)][ins(b, r)] for a D x D pseudo-gate B, one
+// warp: SPLIT lanes per output (xor tree), OPL outputs per lane.  A lane's
+// outputs share each rest r, so their loads are issued together (8 rests
+// unrolled => 8 x OPL independent loads in flight); every output still sums
+// its rests in ascending order.  Result in P (shared memory, by the k == 0 lanes).
+template <int D>
+__device__ __forceinline__ void warp_gather_pt(const Bits &B, const double2 *cts, int N, int lane,
+                                               double2 *P) {
+  constexpr int DD = D * D;
+  constexpr int SPLIT = DD >= 32 ? 1 : 32 / DD;
+  constexpr int OPL = DD >= 32 ? DD / 32 : 1;
+  const int R = 1 << (B.n - B.m);
+  const int k = lane % SPLIT;
+  double2 acc[OPL];
+  int ia[OPL], ib[OPL];
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+    const int o = (lane / SPLIT) + q * (32 / SPLIT);
+    acc[q] = make_double2(0.0, 0.0);
+    ia[q] = B.abits[o / D];
+    ib[q] = B.abits[o % D];
+  }
+#pragma unroll 8
+  for (int r = k; r < R; r += SPLIT) {
+    const int sp = spread_rest(B, r);
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {
+      const double2 v = cts[(long long)(sp | ia[q]) * N + (sp | ib[q])];
+      acc[q].x += v.x;
+      acc[q].y += v.y;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+#pragma unroll
+    for (int off = 1; off < SPLIT; off <<= 1) {
+      acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, off);
+      acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, off);
+    }
+    if (k == 0) P[(lane / SPLIT) + q * (32 / SPLIT)] = acc[q];
+  }
+}
+
 constexpr int kEnvWarps = 4;
 
 template <int D>
@@ -713,9 +756,6 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
   double2 *Vm = Am + D * D;
   const int nact = *A.n_active;
   constexpr int DD = D * D;
-  constexpr int SPLIT = DD >= 32 ? 1 : 32 / DD;  // lanes per output
-  constexpr int OPL = DD >= 32 ? DD / 32 : 1;    // outputs per lane
-  const int R = 1 << (A.b.n - A.b.m);
   const int N = A.N;
   for (int ai = blockIdx.x * kEnvWarps + w; ai < nact; ai += gridDim.x * kEnvWarps) {
     const int s = A.active[ai];
@@ -735,26 +775,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
       }
     } else {
     // P = PT(ct): P[a][b] = sum_r ct[ins(a,r)][ins(b,r)], r ascending per lane
-    const double2 *cts = A.ct + (long long)s * A.ct_stride;
-    const int k = lane % SPLIT;
-#pragma unroll
-    for (int q = 0; q < OPL; q++) {
-      const int o = (lane / SPLIT) + q * (32 / SPLIT);
-      const int a = o / D, b = o % D;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int r = k; r < R; r += SPLIT) {
-        const int sp = spread_rest(A.b, r);
-        const double2 v = cts[(long long)(sp | A.b.abits[a]) * N + (sp | A.b.abits[b])];
-        acc.x += v.x;
-        acc.y += v.y;
-      }
-#pragma unroll
-      for (int off = 1; off < SPLIT; off <<= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-      }
-      if (k == 0) Pm[o] = acc;
-    }
+    warp_gather_pt<D>(A.b, A.ct + (long long)s * A.ct_stride, N, lane, Pm);
     }
     __syncwarp();
     // A = E^dagger with E = (1-beta) PT(peeled ct) + beta u_old^dagger:
@@ -1566,10 +1587,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
   double2 *Am = Pm + 64;
   double2 *Vm = Am + 64;
   const int nact = *A.n_active;
-  const int R = 1 << (A.bw.n - A.bw.m);
   const int N = A.N;
-  constexpr int SPLIT = DD >= 32 ? 1 : 32 / DD;
-  constexpr int OPL = DD >= 32 ? DD / 32 : 1;
   for (int ai = blockIdx.x * kEnvWarps + w; ai < nact; ai += gridDim.x * kEnvWarps) {
     const int s = A.active[ai];
     if (A.part) {
@@ -1586,26 +1604,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
       }
     } else {
     // T = PT_{not W}(ct), rests ascending per lane, fixed xor tree
-    const double2 *cts = A.ct + (long long)s * A.ct_stride;
-    const int k = lane % SPLIT;
-#pragma unroll
-    for (int q = 0; q < OPL; q++) {
-      const int o = (lane / SPLIT) + q * (32 / SPLIT);
-      const int a = o / DW, b = o % DW;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int r = k; r < R; r += SPLIT) {
-        const int sp = spread_rest(A.bw, r);
-        const double2 v = cts[(long long)(sp | A.bw.abits[a]) * N + (sp | A.bw.abits[b])];
-        acc.x += v.x;
-        acc.y += v.y;
-      }
-#pragma unroll
-      for (int off = 1; off < SPLIT; off <<= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-      }
-      if (k == 0) T[o] = acc;
-    }
+    warp_gather_pt<DW>(A.bw, A.ct + (long long)s * A.ct_stride, N, lane, T);
     }
     for (int o = lane; o < DD; o += 32) {
       const double2 one = make_double2(o / DW == o % DW ? 1.0 : 0.0, 0.0);
