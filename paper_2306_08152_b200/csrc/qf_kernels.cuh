@@ -744,6 +744,31 @@ __device__ __forceinline__ void warp_gather_pt(const Bits &B, const double2 *cts
   }
 }
 
+// P[o] = sum over tiles t (ascending) of pp[t * DD + o]: the fused tile
+// partials of a D x D (pseudo-)gate, one warp; a lane's outputs load together,
+// 8 tiles unrolled, so 8 x OPL loads are in flight per lane.
+template <int D>
+__device__ __forceinline__ void warp_sum_parts(const double2 *pp, int tiles, int lane, double2 *P) {
+  constexpr int DD = D * D;
+  constexpr int OPL = DD >= 32 ? DD / 32 : 1;
+  double2 acc[OPL];
+#pragma unroll
+  for (int q = 0; q < OPL; q++) acc[q] = make_double2(0.0, 0.0);
+  if (lane < DD) {
+#pragma unroll 8
+    for (int t = 0; t < tiles; t++) {
+#pragma unroll
+      for (int q = 0; q < OPL; q++) {
+        const double2 v = pp[t * DD + lane + 32 * q];
+        acc[q].x += v.x;
+        acc[q].y += v.y;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < OPL; q++) P[lane + 32 * q] = acc[q];
+  }
+}
+
 constexpr int kEnvWarps = 4;
 
 template <int D>
@@ -763,16 +788,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_env_polar(const EnvArgs A) {
     for (int e = lane; e < DD; e += 32) Uo[e] = u[e];
     if (A.part) {
       // P = sum over the producing sandwich's tiles, tile order
-      const double2 *pp = A.part + (long long)s * A.part_stride;
-      for (int o = lane; o < DD; o += 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int t = 0; t < A.part_tiles; t++) {
-          const double2 v = pp[t * DD + o];
-          acc.x += v.x;
-          acc.y += v.y;
-        }
-        Pm[o] = acc;
-      }
+      warp_sum_parts<D>(A.part + (long long)s * A.part_stride, A.part_tiles, lane, Pm);
     } else {
     // P = PT(ct): P[a][b] = sum_r ct[ins(a,r)][ins(b,r)], r ascending per lane
     warp_gather_pt<D>(A.b, A.ct + (long long)s * A.ct_stride, N, lane, Pm);
@@ -1592,16 +1608,7 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
     const int s = A.active[ai];
     if (A.part) {
       // T = sum over the flushing sandwich's tiles, tile order
-      const double2 *pp = A.part + (long long)s * A.part_stride;
-      for (int o = lane; o < DD; o += 32) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int t = 0; t < A.part_tiles; t++) {
-          const double2 v = pp[t * DD + o];
-          acc.x += v.x;
-          acc.y += v.y;
-        }
-        T[o] = acc;
-      }
+      warp_sum_parts<DW>(A.part + (long long)s * A.part_stride, A.part_tiles, lane, T);
     } else {
     // T = PT_{not W}(ct), rests ascending per lane, fixed xor tree
     warp_gather_pt<DW>(A.bw, A.ct + (long long)s * A.ct_stride, N, lane, T);
@@ -1616,16 +1623,20 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
     for (int j = 0; j < A.nsteps; j++) {
       const GroupStep &g = A.st[j];
       const int d = g.d, dd = d * d;
-      // P = PT_{W \ G}(Lp T Rp)
-      group_mm<DW>(Lp, T, M, lane);
-      group_mm<DW>(M, Rp, Am, lane);  // Am: scratch DW x DW (<= 64)
+      // P = PT_{W \ G}(Lp T Rp)  (first step: Lp = Rp = I, P = PT_{W \ G}(T))
+      const double2 *LTR = T;
+      if (j > 0) {
+        group_mm<DW>(Lp, T, M, lane);
+        group_mm<DW>(M, Rp, Am, lane);  // Am: scratch DW x DW (<= 64)
+        LTR = Am;
+      }
       const int nr = DW / d;
       for (int o = lane; o < dd; o += 32) {
         const int a = o / d, b = o % d;
         double2 acc = make_double2(0.0, 0.0);
         for (int r = 0; r < nr; r++) {
           const int xr = insert_zeros(r, g.gmask);
-          const double2 v = Am[(xr | g.gab[a]) * DW + (xr | g.gab[b])];
+          const double2 v = LTR[(xr | g.gab[a]) * DW + (xr | g.gab[b])];
           acc.x += v.x;
           acc.y += v.y;
         }
