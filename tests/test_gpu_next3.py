@@ -72,3 +72,24 @@ def test_grouped_c5_sample(group):
     gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(), init,
                               R=2, max_iters=2, engine=qf.QF_ENGINE_STREAM)
     _compare(gpu, orc, idx, 2, 2 ** w.n)
+
+
+@pytest.mark.parametrize("group", [3], indirect=True)
+@pytest.mark.parametrize("n,p,seed", [(8, 9, 64), (9, 7, 65)])
+def test_grouped_fused_partials(group, n, p, seed, monkeypatch):
+    """QF_GROUP_FUSE=1: a d = 8 group flush on the row-tile kernel leaves the
+    next group's T as tile partials (W as a pseudo-gate) and k_group sums them
+    instead of gathering; same oracle bar (DESIGN 9e; off by default)."""
+    monkeypatch.setenv("QF_GROUP_FUSE", "1")
+    locs, kinds, cm = qfgen.random_template(n, p, seed=seed, const_frac=0.2)
+    V = qfgen.haar(qfgen.stream_key(seed, qfgen.PURPOSE_TARGET, 0, 0), 2 ** n)[0]
+    init = qfgen.initial_gates(n, locs, kinds, 5300 + seed, 0, 6)
+    gpu, orc, idx = _run_pair(n, locs, kinds, cm, V, init, R=4, max_iters=4,
+                              engine=qf.QF_ENGINE_STREAM)
+    _compare(gpu, orc, idx, 4, 2 ** n)
+    # the partial path really ran: the gather path sums in another order
+    monkeypatch.setenv("QF_GROUP_FUSE", "0")
+    c = qf.Circuit(n, locs, kinds, cm)
+    ref = qf.qf_instantiate(c, V, init, max_iters=4, engine=qf.QF_ENGINE_STREAM)
+    assert not np.array_equal(gpu.gates, ref.gates)
+    assert np.max(np.abs(gpu.gates - ref.gates)) < 1e-11
