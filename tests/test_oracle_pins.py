@@ -18,7 +18,9 @@ What pins each oracle function (none of these retypes the oracle's formula):
                       after every sweep; |Tr| non-decreasing over single
                       updates; |Tr| <= N; special cases
                       (self-target fixed point, whole-register gate, product
-                      target, C1 KAK universality, global phase invariance).
+                      target, C1 KAK universality, global phase invariance);
+                      the half-sweep order p..1 then 1..p by a
+                      dense brute-force sweep with LAPACK Procrustes updates.
   terminate        -- hand-built cost sequences for every verdict.
 """
 import json
@@ -267,6 +269,57 @@ def test_init_and_sweep_bookkeeping(orc, seed):
         U2 = dense_circuit(n, locs, _mats(locs, kinds, cm, g2))
         assert np.abs(ct - U2 @ V.conj().T).max() < 1e-11
         g = g2
+
+
+def _brute_sweep(n, locs, kinds, mats, V, order):
+    """One sweep by brute force: at every step k of `order` the environment of
+    gate k is built densely by linearity from the CURRENT gates,
+    and a VARIABLE gate is replaced by the textbook Procrustes maximiser of
+    Re Tr(E u) from numpy's LAPACK SVD.  Returns the gates and
+    Tr(V^dag U) after every step."""
+    mats = [np.array(m) for m in mats]
+    log = []
+    for k in order:
+        if kinds[k] == qfgen.VARIABLE:
+            Ue, _, Vh = np.linalg.svd(_brute_env(n, locs, mats, V, k))
+            mats[k] = Vh.conj().T @ Ue.conj().T
+        log.append(np.trace(V.conj().T @ dense_circuit(n, locs, mats)))
+    return mats, np.array(log)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_sweep_order_brute_force(orc, seed):
+    """TwoSidedSweep visits k = p..1 first ("reversed"), then
+    k = 1..p, each update using the gates as already updated in this
+    sweep.  The oracle's per-step traces and final gates must
+    equal a dense brute-force sweep in that order; the swapped halves, the
+    forward half alone first, or updates from stale gates all give other
+    values (checked below, so the pin is sensitive to those mistakes); an
+    update from stale gates would not match the brute force, which always
+    builds the environment from the current ones."""
+    n = 3
+    locs = [(0, 1), (1, 2), (2, 0), (1,)]
+    kinds = [qfgen.VARIABLE, qfgen.VARIABLE, qfgen.CONSTANT, qfgen.VARIABLE]
+    cm = [None, None, qfgen.CNOT, None]
+    rng = np.random.default_rng(500 + seed)
+    V = haar_np(rng, 2 ** n)
+    g = qfgen.initial_gates(n, locs, kinds, 70 + seed, 0, 1)[0]
+    mats = _mats(locs, kinds, cm, g)
+    p = len(locs)
+    order = list(range(p - 1, -1, -1)) + list(range(p))
+    ref_mats, ref_log = _brute_sweep(n, locs, kinds, mats, V, order)
+    C = _circ(orc, n, locs, kinds, cm)
+    _, g2, log = orc.sweep(C, orc.init_ct(C, V, g), g, log=True)
+    assert np.abs(log - ref_log).max() < 1e-11
+    got = _mats(locs, kinds, cm, g2)
+    for k in range(p):
+        assert np.abs(got[k] - ref_mats[k]).max() < 1e-10
+    # sensitivity: plausible wrong schedules disagree with the oracle
+    for bad in (list(range(p)) + list(range(p - 1, -1, -1)),      # halves swapped
+                list(range(p)) * 2,                                # forward only
+                list(range(p - 1, -1, -1)) * 2):                   # backward only
+        _, bad_log = _brute_sweep(n, locs, kinds, mats, V, bad)
+        assert np.abs(log - bad_log).max() > 1e-6
 
 
 @pytest.mark.parametrize("seed", range(5))
