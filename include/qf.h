@@ -131,6 +131,16 @@ typedef struct {
   int32_t batch_policy;   /* qf_batch_policy (default QF_BATCH_PER_START)   */
   qf_batch_reduce_fn batch_reduce; /* NULL: this call is the whole batch   */
   void *batch_user;       /* passed to batch_reduce                         */
+  /* Seeded starts ("controlled by a seed"): when the
+   * caller passes initial == NULL, start s of this call (global index
+   * start_offset + s) begins from Haar-random VARIABLE gates and uniform
+   * R_z angles drawn on the device from SplitMix64 counter streams keyed by
+   * (seed, purpose 1, start_offset + s, gate index) -- the recipe of the
+   * input module qfgen, so the gates depend only
+   * on (seed, global start, gate): shard a job by giving each call its own
+   * start_offset.  Ignored when initial is given. */
+  uint64_t seed;          /* default 0                                      */
+  int64_t start_offset;   /* >= 0, default 0                                */
 } qf_params;
 
 /* Per-start summary, 16 bytes (allgathered across ranks). */
@@ -178,10 +188,11 @@ int qf_circuit_num_qubits(qf_circuit_t c);
 
 /* Blocking instantiation from HOST buffers (the end-to-end call; host<->
  * device copies happen inside).  target: N*N complex; initial: num_starts
- * x var_doubles doubles (required; the seeded generator lives in the
- * caller's input module).  Runs on the current
- * CUDA device.  Errors: QF_E_ARG, QF_E_NOT_UNITARY (target, initial gates;
- * 1e-9), QF_E_OOM, QF_E_CUDA. */
+ * x var_doubles doubles, or NULL for seeded starts generated on the device
+ * from (p->seed, p->start_offset) (see qf_params; Alg. 1 from a start
+ * count alone).  Runs on the current CUDA device.  Errors: QF_E_ARG,
+ * QF_E_NOT_UNITARY (target, given initial gates; 1e-9), QF_E_OOM,
+ * QF_E_CUDA. */
 qf_status qf_instantiate(qf_circuit_t c, const double *target,
                          const double *initial, const qf_params *p,
                          qf_result_t *out);
@@ -220,7 +231,8 @@ size_t qf_workspace_size(qf_circuit_t c, const qf_params *p);
 /* Blocking instantiation from DEVICE buffers already resident in HBM (the
  * kernel-throughput call; no host<->device copies of inputs).
  *   d_target   device, N*N complex (read only)
- *   d_initial  device, num_starts x var_doubles (read only)
+ *   d_initial  device, num_starts x var_doubles (read only), or NULL for
+ *              seeded starts from (p->seed, p->start_offset)
  *   d_workspace / workspace_bytes  device scratch >= qf_workspace_size
  *   stream     cudaStream_t (as void*), NULL = the legacy default stream
  *   d_gates_out   device, num_starts x var_doubles, final gates (nullable)

@@ -71,6 +71,8 @@ class qf_params(ctypes.Structure):
         ("batch_policy", ctypes.c_int32),
         ("batch_reduce", BATCH_REDUCE_FN),
         ("batch_user", ctypes.c_void_p),
+        ("seed", ctypes.c_uint64),
+        ("start_offset", ctypes.c_int64),
     ]
 
 
@@ -278,16 +280,24 @@ def _collect_trace(h, res: Result, count, R, var):
     res.cost_hist, res.gates_hist = ch, gh
 
 
-def qf_instantiate(circ: Circuit, target, initial, record_starts=None, record_sweeps=0,
-                   **params) -> Result:
-    """Blocking instantiation from host buffers (the end-to-end call)."""
-    initial = np.ascontiguousarray(initial, dtype=np.float64)
-    S = initial.shape[0]
-    assert initial.shape == (S, circ.var_doubles)
+def qf_instantiate(circ: Circuit, target, initial=None, record_starts=None, record_sweeps=0,
+                   num_starts=None, **params) -> Result:
+    """Blocking instantiation from host buffers (the end-to-end call).
+    initial=None: `num_starts` seeded starts generated on the device from
+    params seed / start_offset (qf.h qf_params)."""
+    if initial is None:
+        S = int(num_starts)
+        iptr = None
+    else:
+        initial = np.ascontiguousarray(initial, dtype=np.float64)
+        S = initial.shape[0]
+        assert initial.shape == (S, circ.var_doubles)
+        assert num_starts is None or num_starts == S
+        iptr = initial.ctypes.data_as(_D)
     p, keep = _make_params(S, record_starts, record_sweeps, **params)
     t = _cplx(target)
     h = _VP()
-    _check(lib().qf_instantiate(circ.h, t.ctypes.data_as(_D), initial.ctypes.data_as(_D),
+    _check(lib().qf_instantiate(circ.h, t.ctypes.data_as(_D), iptr,
                                 ctypes.byref(p), ctypes.byref(h)))
     try:
         res = _collect(h, circ.var_doubles, True)
@@ -352,16 +362,19 @@ def qf_instantiate_device(circ: Circuit, d_target, d_initial, workspace, stream=
     """Blocking instantiation from device-resident torch tensors.
 
     d_target: complex128 (N, N) or float64 (N, N, 2) CUDA tensor; d_initial:
-    float64 (S, var) CUDA tensor; workspace: uint8 CUDA tensor of at least
+    float64 (S, var) CUDA tensor, or None for `num_starts` seeded starts
+    (params seed / start_offset); workspace: uint8 CUDA tensor of at least
     qf_workspace_size bytes; stream: torch.cuda.Stream (default: current)."""
     import torch
 
-    S = int(d_initial.shape[0])
+    S = int(d_initial.shape[0]) if d_initial is not None else int(params.pop("num_starts"))
+    params.pop("num_starts", None)
     p, keep = _make_params(S, record_starts, record_sweeps, **params)
     st = stream if stream is not None else torch.cuda.current_stream()
     h = _VP()
     _check(lib().qf_instantiate_device(
-        circ.h, _VP(d_target.data_ptr()), _VP(d_initial.data_ptr()), ctypes.byref(p),
+        circ.h, _VP(d_target.data_ptr()),
+        _VP(d_initial.data_ptr()) if d_initial is not None else None, ctypes.byref(p),
         _VP(workspace.data_ptr()), int(workspace.numel() * workspace.element_size()),
         _VP(st.cuda_stream), _VP(d_gates_out.data_ptr()) if d_gates_out is not None else None,
         _VP(d_summary_out.data_ptr()) if d_summary_out is not None else None,
@@ -402,7 +415,8 @@ def qf_instantiate_ptr(circ: Circuit, target_ptr: int, initial_ptr: int, S: int,
     the call's qf_stats plus the best start's summary (bench e2e leg)."""
     p, _ = _make_params(S, **params)
     h = _VP()
-    _check(lib().qf_instantiate(circ.h, ctypes.cast(target_ptr, _D), ctypes.cast(initial_ptr, _D),
+    _check(lib().qf_instantiate(circ.h, ctypes.cast(target_ptr, _D),
+                                ctypes.cast(initial_ptr, _D) if initial_ptr else None,
                                 ctypes.byref(p), ctypes.byref(h)))
     try:
         st = qf_stats()

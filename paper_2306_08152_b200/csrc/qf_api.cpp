@@ -139,6 +139,7 @@ qf_status check_params(const qf_circuit_s *c, const qf_params *p) {
   if (!(p->diff_tol_a >= 0.0) || !(p->diff_tol_r >= 0.0) || !(p->long_diff_r >= 0.0))
     return fail(QF_E_ARG, "diff_tol_a, diff_tol_r and long_diff_r must be >= 0");
   if (!(p->beta >= 0.0 && p->beta <= 1.0)) return fail(QF_E_ARG, "beta must lie in [0, 1]");
+  if (p->start_offset < 0) return fail(QF_E_ARG, "start_offset must be >= 0");
   if (p->engine != QF_ENGINE_AUTO && p->engine != QF_ENGINE_STREAM &&
       p->engine != QF_ENGINE_RESIDENT)
     return fail(QF_E_ARG, "engine must be QF_ENGINE_AUTO, _STREAM or _RESIDENT");
@@ -288,7 +289,6 @@ qf_status qf_instantiate_device(qf_circuit_t c, const double *d_target, const do
   qf_status s = check_params(c, p);
   if (s != QF_OK) return s;
   if (!d_target) return fail(QF_E_ARG, "target is NULL");
-  if (!d_initial && c->var_doubles > 0) return fail(QF_E_ARG, "initial is NULL");
   qf_result_s *r = nullptr;
   if (out) {
     r = new (std::nothrow) qf_result_s();
@@ -316,13 +316,13 @@ qf_status qf_instantiate(qf_circuit_t c, const double *target, const double *ini
   qf_status s = check_params(c, p);
   if (s != QF_OK) return s;
   if (!target) return fail(QF_E_ARG, "target is NULL");
-  if (!initial && c->var_doubles > 0)
-    return fail(QF_E_ARG, "initial is NULL (pass seeded gates from the input module)");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev < 1) return fail(QF_E_CUDA, "no CUDA device available");
   const size_t N = (size_t)1 << c->n;
-  const size_t tbytes = N * N * 16, ibytes = (size_t)p->num_starts * c->var_doubles * 8;
+  // initial == NULL: seeded starts generated on the device (no copy)
+  const size_t tbytes = N * N * 16,
+               ibytes = initial ? (size_t)p->num_starts * c->var_doubles * 8 : 0;
   const size_t wbytes = qf::engine_workspace_size(*c, *p);
   qf::retain_device_pool();
   cudaStream_t st = nullptr;
@@ -349,8 +349,8 @@ qf_status qf_instantiate(qf_circuit_t c, const double *target, const double *ini
     qf::EngineOut eo;
     eo.host = r;
     eo.host_all_gates = true;
-    s = qf::engine_run(*c, reinterpret_cast<double *>(d_t), reinterpret_cast<double *>(d_i), *p,
-                       d_w, wbytes, st, eo);
+    s = qf::engine_run(*c, reinterpret_cast<double *>(d_t),
+                       initial ? reinterpret_cast<double *>(d_i) : nullptr, *p, d_w, wbytes, st, eo);
   }
   cudaFreeAsync(buf, st);
   cudaStreamSynchronize(st);

@@ -108,6 +108,97 @@ __global__ void k_check_target(const double2 *V, int N, double tol, int *bad) {
   }
 }
 
+// ------------------------------------------------------------------ seeded starts
+// Initial unitaries "controlled by a seed" (reading R12): Haar on
+// U(d) for VARIABLE gates, R_z(theta) with theta uniform in [0, 2 pi) for RZ
+// gates, from counter-based SplitMix64 streams keyed by (seed, purpose = 1,
+// GLOBAL start index, gate index), so a start's gates depend only on those
+// (sharding-invariant).  The same counter generator as the input module
+// `qfgen` (each side implements it; SURVEY Sec. 8b "keyed Haar starts"):
+//   u_c = ((splitmix64(key + c G2) >> 11) + 1/2) 2^-53,  c = 0, 1, ...
+//   z[r][k] = sqrt(-2 ln u_{2i}) e^{i 2 pi u_{2i+1}} / sqrt 2,  i = r d + k
+//   Q = twice-iterated modified Gram-Schmidt of z's columns (= the Q of QR
+//       with a positive real R diagonal, Mezzadri's phase fix).
+// Products and sums are rounded one by one (no FMA), in numpy's order.
+__device__ __forceinline__ unsigned long long sm64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double uni64(unsigned long long key, unsigned long long c) {
+  const unsigned long long x = sm64(key + c * 0xD1B54A32D192ED03ull);
+  return __dmul_rn(__dadd_rn((double)(x >> 11), 0.5), 1.0 / 9007199254740992.0);
+}
+
+// conj(a) * b and a * b with separately rounded products (numpy complex ops)
+__device__ __forceinline__ double2 cmul_cj_rn(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(-a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(-a.y, b.x)));
+}
+__device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+
+// One thread per (start, parameterised gate); tab[g] = (gate index k,
+// offset in doubles, d, kind).  Writes start s's gates at G + s var_doubles.
+__global__ void k_seeded_starts(double *G, long long S, long long start_offset,
+                                unsigned long long seed, int nvar, const int4 *tab,
+                                int var_doubles) {
+  const long long total = S * nvar;
+  const double twopi = 2.0 * 3.141592653589793;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long s = e / nvar;
+    const int4 g = tab[e % nvar];
+    unsigned long long key = sm64(seed);
+    key = sm64(key ^ 1ull);  // purpose: initial unitaries of the multistarts
+    key = sm64(key ^ (unsigned long long)(start_offset + s));
+    key = sm64(key ^ (unsigned long long)g.x);
+    double2 *u = reinterpret_cast<double2 *>(G + s * var_doubles + g.y);
+    if (g.w == QF_GATE_RZ) {
+      const double th = __dmul_rn(twopi, uni64(key, 0));
+      u[0] = make_double2(1.0, 0.0);
+      u[1] = u[2] = make_double2(0.0, 0.0);
+      u[3] = make_double2(cos(th), sin(th));
+      continue;
+    }
+    const int d = g.z;
+    double2 q[64];
+    for (int i = 0; i < d * d; i++) {
+      const double u1 = uni64(key, 2 * i), u2 = uni64(key, 2 * i + 1);
+      const double r = sqrt(__dmul_rn(-2.0, log(u1))), a = __dmul_rn(twopi, u2);
+      q[i] = make_double2(__ddiv_rn(__dmul_rn(r, cos(a)), 1.4142135623730951),
+                          __ddiv_rn(__dmul_rn(r, sin(a)), 1.4142135623730951));
+    }
+    for (int j = 0; j < d; j++) {  // column j of q in place: q[r d + j]
+      for (int rep = 0; rep < 2; rep++)
+        for (int i = 0; i < j; i++) {
+          double2 acc = cmul_cj_rn(q[i], q[j]);
+          for (int r = 1; r < d; r++) {
+            const double2 t = cmul_cj_rn(q[r * d + i], q[r * d + j]);
+            acc = make_double2(__dadd_rn(acc.x, t.x), __dadd_rn(acc.y, t.y));
+          }
+          for (int r = 0; r < d; r++) {
+            const double2 t = cmul_rn(acc, q[r * d + i]);
+            q[r * d + j] = make_double2(__dsub_rn(q[r * d + j].x, t.x),
+                                        __dsub_rn(q[r * d + j].y, t.y));
+          }
+        }
+      double nn = __dadd_rn(__dmul_rn(q[j].x, q[j].x), __dmul_rn(q[j].y, q[j].y));
+      for (int r = 1; r < d; r++)
+        nn = __dadd_rn(nn, __dadd_rn(__dmul_rn(q[r * d + j].x, q[r * d + j].x),
+                                     __dmul_rn(q[r * d + j].y, q[r * d + j].y)));
+      const double inv = sqrt(nn);
+      for (int r = 0; r < d; r++)
+        q[r * d + j] = make_double2(__ddiv_rn(q[r * d + j].x, inv), __ddiv_rn(q[r * d + j].y, inv));
+    }
+    for (int i = 0; i < d * d; i++) u[i] = q[i];
+  }
+}
+
 // unitarity of every VARIABLE initial gate: one thread per (start, gate)
 __global__ void k_check_gates(const double *G, long long S, int nvar, const int2 *tab,
                               int var_doubles, double tol, int *bad) {
@@ -220,7 +311,7 @@ std::pair<int, int> row_tiles(int n, int m) {
 struct Layout {
   size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
       rec_slot, rec_starts, rec_cost, rec_gates, summary, best, part, tpart, vstore, vslots,
-      gdesc, plat, gops, bcnt, total;
+      gdesc, plat, gops, bcnt, gkey, total;
   long long vstride;  // complex per start in vstore (sum over VARIABLE gates of 2 d^2)
   int nvslots;
   int ring;
@@ -244,6 +335,7 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
   L.vdag = take(N * N * 16);
   L.cmats = take(std::max<size_t>(1, c.const_mats.size()) * 8);
   L.gtab = take((size_t)std::max(1, c.p) * 8);
+  L.gkey = take((size_t)std::max(1, c.p) * 16);  // seeded starts: (gate, offset, d, kind)
   L.hist = take(S * (size_t)L.ring * 8);
   L.delta = take(S * 8);
   L.iters = take(S * 4);
@@ -1047,7 +1139,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   k_vdag<<<g1, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), E.vdag(), N);
   k_check_target<<<g1, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), N, 1e-9, E.bad());
   E.launches += 2;
-  if (!tab.empty()) {
+  if (!tab.empty() && d_initial != nullptr) {
     const long long tot = (long long)S * tab.size();
     const int g2 = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, E.nsm * 16));
     k_check_gates<<<g2, 256, 0, st>>>(d_initial, S, (int)tab.size(),
@@ -1056,9 +1148,25 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     E.launches++;
   }
   QF_CHECK(cudaGetLastError());
-  if (c.var_doubles > 0)
+  if (c.var_doubles > 0 && d_initial != nullptr) {
     QF_CHECK(cudaMemcpyAsync(E.gates(), d_initial, (size_t)S * c.var_doubles * 8,
                              cudaMemcpyDeviceToDevice, st));
+  } else if (c.var_doubles > 0) {  // seeded starts (initial == NULL), generated in place
+    std::vector<int4> keys;
+    for (int k = 0; k < c.p; k++)
+      if (c.kind[k] != QF_GATE_CONSTANT)
+        keys.push_back(make_int4(k, c.var_off[k], 1 << c.arity[k], c.kind[k]));
+    QF_CHECK(cudaMemcpyAsync(W + E.L.gkey, keys.data(), keys.size() * sizeof(int4),
+                             cudaMemcpyHostToDevice, st));
+    h2d += (long long)(keys.size() * sizeof(int4));
+    const long long tot = (long long)S * keys.size();
+    const int g3 = (int)std::max<long long>(1, std::min<long long>((tot + 127) / 128, E.nsm * 32));
+    k_seeded_starts<<<g3, 128, 0, st>>>(E.gates(), S, p.start_offset, p.seed, (int)keys.size(),
+                                        reinterpret_cast<const int4 *>(W + E.L.gkey),
+                                        c.var_doubles);
+    E.launches++;
+    QF_CHECK(cudaGetLastError());
+  }
   int *rec_slot = reinterpret_cast<int *>(W + E.L.rec_slot);
   k_iota<<<std::max(1, std::min((S + 255) / 256, E.nsm * 4)), 256, 0, st>>>(E.active(), E.n_active(),
                                                                              S, rec_slot);

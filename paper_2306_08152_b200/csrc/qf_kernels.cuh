@@ -551,7 +551,8 @@ __device__ __forceinline__ void warp_mm(const double2 *Am, const double2 *Bm, do
 // steeper quintic p(s) = 3.4445 s - 4.7750 s^3 + 2.0315 s^5 (maps (0, 1.2]
 // into (0, 1.2], slope 3.44 at 0) instead.  Stops one step after
 // max |Y - I| <= 1e-5 (error then ~(1e-5)^3).  Returns false if A is zero or
-// not finite, or has not converged after 48 steps (A singular or near it);
+// not finite, or some |Y - I| entry is still > 0.55 after 16 steps (A
+// singular or near it), or it has not converged after 48 steps;
 // Xm then holds A or an iterate with the same polar factor and the caller
 // finishes with Jacobi.
 // Buffers: X in Xm (in place), Y in Ym, W in Wm; result copied to U (may
@@ -625,6 +626,11 @@ __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U,
       code = cq > code ? cq : code;
     }
     code = __reduce_max_sync(0xffffffffu, code);
+    // a singular value still below ~0.45 after 8 steep + 8 cubic steps was
+    // below ~2e-7 sigma_max at the start (growth >= 3.44^8 1.875^8): A is
+    // singular or nearly so, and Newton-Schulz would spend its remaining
+    // steps creeping (an exact zero never moves) -- hand over to Jacobi now
+    if (code == 2u && it >= 16) break;
     done = code == 0;
     if (fast) fast = it < 8 && code == 2;
     const double ca = fast ? 3.4445 : 1.875, cb = fast ? -4.7750 : -1.25,

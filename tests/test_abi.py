@@ -71,7 +71,7 @@ def test_param_validation_precedes_device():
     g = w.initial()
     for bad, status in (({"beta": 1.5}, qf.QF_E_ARG), ({"dist_tol": 0.0}, qf.QF_E_ARG),
                         ({"max_iters": -1}, qf.QF_E_ARG), ({"reset_iters": 0}, qf.QF_E_ARG),
-                        ({"batch_policy": 2}, qf.QF_E_ARG),
+                        ({"batch_policy": 2}, qf.QF_E_ARG), ({"start_offset": -1}, qf.QF_E_ARG),
                         ({"batch_policy": qf.QF_BATCH_PAPER, "engine": qf.QF_ENGINE_RESIDENT},
                          qf.QF_E_ARG)):
         with pytest.raises(qf.QfError) as e:
@@ -88,6 +88,9 @@ def test_no_device_fails_loudly():
     c = qf.Circuit.from_workload(w)
     with pytest.raises(qf.QfError) as e:
         qf.qf_instantiate(c, w.target_unitary(), w.initial())
+    assert e.value.status == qf.QF_E_CUDA
+    with pytest.raises(qf.QfError) as e:  # seeded starts: no host fallback either
+        qf.qf_instantiate(c, w.target_unitary(), None, num_starts=4, seed=1)
     assert e.value.status == qf.QF_E_CUDA
 
 

@@ -12,6 +12,7 @@ import qfgen
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-10  # north_star tolerance, absolute
+from conftest import BORDERLINE  # noqa: E402  (R21 starts, summarised at session end)
 
 
 def _orc_circ(n, locs, kinds, cm):
@@ -75,9 +76,23 @@ def _compare(gpu, orc_P, idx, R, N, check_final=True):
         assert (gd[j] < 1e-8) == (orc.delta[j] < 1e-8)
         borderline.append((int(idx[j]), int(gv[j]), int(orc.verdict[j]), float(margin)))
     assert np.array_equal(gd < 1e-8, orc.delta < 1e-8)  # success, every start
+    # north_star: the converged-or-not verdict agrees on every start.  The one
+    # exception the arithmetic forces (R21): a start that stagnates
+    # at Delta ~ dist_tol, where the short-plateau threshold diff_tol_r * Delta
+    # ~ 1e-15 lies below the fp64 resolution of Delta, so one side's plateau
+    # test fires and the other's Delta drifts under dist_tol a few sweeps
+    # later.  Such a flip must be rounding-borderline (margin above), succeed
+    # on both sides, and be rare; each one is listed in the session summary.
+    flips = [(int(idx[j]), int(gv[j]), int(gi[j]), float(gd[j]), int(orc.verdict[j]),
+              int(orc.iters[j]), float(orc.delta[j])) for j in range(len(idx))
+             if (gv[j] == qf.QF_CONVERGED) != (orc.verdict[j] == qf.QF_CONVERGED)]
+    for f in flips:
+        assert f[0] in [b[0] for b in borderline] and f[3] < 1e-8 and f[6] < 1e-8, f
+    assert len(flips) <= max(1, len(idx) // 32), flips
     if borderline:
         print("rounding-borderline starts (start, gpu verdict, oracle verdict, margin):",
               borderline)
+    BORDERLINE.append((len(idx), borderline, flips))
     assert len(borderline) <= max(1, len(idx) // 4), borderline
     if R:
         ch_g, ch_o = gpu.cost_hist[:, :R], orc.cost_hist[:, :R]
@@ -211,6 +226,23 @@ def test_parity_C5_capped():
     gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(),
                               w.initial(), R=2, sample=sample, max_iters=2)
     _compare(gpu, orc, idx, 2, 2 ** w.n)
+
+
+def test_parity_C5_spread_to_verdict():
+    """C5 (the HBM-regime config) on 16 starts spread over the 8192 global
+    starts: every sweep's Delta and every gate entry for the first 10 sweeps
+    within 1e-10 of the oracle, and each start run to its verdict on both
+    sides (north_star).  The GPU runs only these 16 starts -- per-start
+    results do not depend on batch composition
+    (test_sharding_invariance_bitwise) -- on the streaming engine bench.py's
+    C5 probe uses."""
+    w = qfgen.workload("C5")
+    starts = np.linspace(0, w.starts - 1, 16).astype(int)
+    init = np.concatenate([w.initial(int(s), 1) for s in starts])
+    gpu, orc, idx = _run_pair(w.n, w.locs, w.kinds, w.const_mats, w.target_unitary(), init,
+                              R=10, max_iters=w.max_iters)
+    _compare(gpu, orc, idx, 10, 2 ** w.n)
+    assert np.all(gpu.verdict != qf.QF_RUNNING) and np.all(gpu.iters > 10)
 
 
 # ------------------------------------------------------------------ edge cases
