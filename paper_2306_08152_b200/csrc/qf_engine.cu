@@ -38,6 +38,21 @@ int resident_threads(int n) {
   return std::max(32, std::min(128, items));
 }
 
+// the WIDE resident variant (256 threads, FP64-MMA d = 4 sandwich): n = 5, 6
+// and no gate wider than 2 qubits; QF_RES_WIDE=0 disables (A/B)
+bool resident_wide(int n, int maxm) {
+  const int env = getenv("QF_RES_WIDE") ? atoi(getenv("QF_RES_WIDE")) : 1;
+  return env != 0 && kResDmma4 && n >= 5 && maxm == 2;
+}
+int resident_threads(int n, int maxm) { return resident_wide(n, maxm) ? 256 : resident_threads(n); }
+
+// dynamic shared memory of k_resident: the tensor, 8 operand slots (16 complex
+// each for WIDE, else 64), two MMA tile tables and (WIDE) the 16 x 16 T
+size_t resident_smem(int N, bool wide) {
+  return (size_t)N * N * 16 + 8 * (wide ? 16 : 64) * 16 + kResTabBytes +
+         (wide ? 256 * 16 + ((sizeof(WDesc) + 15) & ~size_t(15)) : 0);
+}
+
 // CUDA-event timing of individual launches (qf_params.profile = 1): a ring of
 // event pairs, harvested when a slot is reused and at the end of the call.
 struct Profiler {
@@ -311,7 +326,7 @@ std::pair<int, int> row_tiles(int n, int m) {
 struct Layout {
   size_t ct, gates, scratch, vdag, cmats, gtab, hist, delta, iters, verdict, active, counters,
       rec_slot, rec_starts, rec_cost, rec_gates, summary, best, part, tpart, vstore, vslots,
-      gdesc, plat, gops, bcnt, gkey, total;
+      gdesc, plat, gops, bcnt, gkey, wdesc, total;
   long long vstride;  // complex per start in vstore (sum over VARIABLE gates of 2 d^2)
   int nvslots;
   int ring;
@@ -363,6 +378,7 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
   L.vstore = take(std::max<size_t>(1, S * (size_t)L.vstride) * 16);
   L.vslots = take((size_t)std::max(1, L.nvslots) * 8);
   L.gdesc = take((size_t)std::max(1, c.p) * sizeof(GateDesc));
+  L.wdesc = take((size_t)std::max(1, 2 * c.p) * sizeof(WDesc));  // WIDE resident transitions
   L.plat = take(S * 4);
   L.gops = take(S * 128 * 16);  // grouped steps: Lp, Rp (<= 8 x 8) per start
   L.bcnt = take((3 * ((size_t)std::max(0, p.max_iters) + 1) + 2) * 4);  // resident batch counts
@@ -1058,6 +1074,7 @@ ResidentKernel resident_kernel(int n, int maxm) {
   if (n <= 4)
     return maxm == 1 ? k_resident<2, false, true> : maxm == 2 ? k_resident<4, false, true>
                                                             : k_resident<8, false, true>;
+  if (resident_wide(n, maxm)) return k_resident<4, false, false, true>;
   return maxm == 1 ? k_resident<2, false> : maxm == 2 ? k_resident<4, false> : k_resident<8, false>;
 }
 
@@ -1068,6 +1085,49 @@ bool resident_batch_default() {
 }
 
 // gate descriptors of the resident engine (voff: warm-start slots or null)
+// GF(2) rank of three-bit vectors
+static int rank3(int a, int b, int c) {
+  int v[3] = {a, b, c}, r = 0;
+  for (int bit = 0; bit < 3; bit++) {
+    int piv = -1;
+    for (int i = r; i < 3; i++)
+      if ((v[i] >> bit) & 1) piv = i;
+    if (piv < 0) continue;
+    std::swap(v[r], v[piv]);
+    for (int i = 0; i < 3; i++)
+      if (i != r && ((v[i] >> bit) & 1)) v[i] ^= v[r];
+    r++;
+  }
+  return r;
+}
+
+// Rest-index bit whose basis column pairs the two column rests of a d = 4
+// FP64-MMA sandwich tile (res_sandwich_dmma4): the lowest basis bit w outside
+// the location for which the tile's loads (row bits u, v; column bit w) and
+// stores (row bit u, column bits v, w) both hit 8 distinct bank groups under
+// the resident swizzle (sidx).  u, v: basis bits of location[0], location[1].
+static int pick_pair_bit(const Bits &b) {
+  if (b.m != 2 || b.n < 3) return 0;
+  const int u = __builtin_ctz(b.abits[2]), v = __builtin_ctz(b.abits[1]);
+  auto rowv = [](int p) { return p < 6 ? kSwRow[p] : 0; };
+  auto colv = [](int p) { return p < 3 ? 1 << p : (p < 6 ? kSwCol[p - 3] : 0); };
+  for (int t = 0; t < b.n - b.m; t++) {
+    const int w = b.rest_pos[t];
+    if (rank3(rowv(u), rowv(v), colv(w)) == 3 && rank3(rowv(u), colv(v), colv(w)) == 3) return t;
+  }
+  return 0;
+}
+
+// W-space descriptors of the 2p transitions j -> j + 1 of a sweep (WIDE
+// resident engine; step j: gate p-1-j backward for j < p, gate j-p forward)
+std::vector<WDesc> make_wdescs(const std::vector<GateDesc> &gd) {
+  const int p = (int)gd.size(), steps = 2 * p;
+  std::vector<WDesc> out((size_t)std::max(1, steps));
+  auto gate_of = [&](int j) { return j >= p ? j - p : p - 1 - j; };
+  for (int j = 0; j + 1 < steps; j++) res_make_wdesc(gd[gate_of(j)], gd[gate_of(j + 1)], out[j]);
+  return out;
+}
+
 std::vector<GateDesc> make_gdesc(const qf_circuit_s &c, const std::vector<int> *voff) {
   std::vector<GateDesc> gd(c.p);
   for (int k = 0; k < c.p; k++) {
@@ -1081,6 +1141,7 @@ std::vector<GateDesc> make_gdesc(const qf_circuit_s &c, const std::vector<int> *
     g.voff = voff && g.kind != 1 ? (*voff)[k] : 0;
     for (int a = 0; a < 8; a++) g.abits[a] = a < b.d ? b.abits[a] : 0;
     for (int q = 0; q < kMaxQubits; q++) g.rest_pos[q] = q < c.n - b.m ? b.rest_pos[q] : 0;
+    g.pbit = pick_pair_bit(b);
   }
   return gd;
 }
@@ -1226,10 +1287,10 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
     const auto kern = resident_kernel(c.n, maxm);
-    const size_t smem = (size_t)N * N * 16 + 8 * 64 * 16;
+    const size_t smem = resident_smem(N, resident_wide(c.n, maxm));
     int per_sm = 0;
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, resident_threads(c.n), smem));
+    QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, resident_threads(c.n, maxm), smem));
     resident_batch = (long long)S <= (long long)per_sm * E.nsm;
   }
   const bool resident = p.engine == QF_ENGINE_RESIDENT || resident_batch ||
@@ -1252,6 +1313,10 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     QF_CHECK(cudaMemcpyAsync(W + E.L.gdesc, gd.data(), gd.size() * sizeof(GateDesc),
                              cudaMemcpyHostToDevice, st));
     h2d += (long long)(gd.size() * sizeof(GateDesc));
+    const std::vector<WDesc> wdt = make_wdescs(gd);
+    QF_CHECK(cudaMemcpyAsync(W + E.L.wdesc, wdt.data(), wdt.size() * sizeof(WDesc),
+                             cudaMemcpyHostToDevice, st));
+    h2d += (long long)(wdt.size() * sizeof(WDesc));
     int *counter = E.n_active() + 2;
     QF_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
     ResidentArgs A{};
@@ -1264,10 +1329,14 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.cmats = E.cmats();
     A.gates = reinterpret_cast<double2 *>(E.gates());
     A.gstride = c.var_doubles / 2;
+    A.wdt = reinterpret_cast<const WDesc *>(W + E.L.wdesc);
     A.vstore = E.warm ? reinterpret_cast<double2 *>(W + E.L.vstore) : nullptr;
     A.vstride = E.L.vstride;
     A.counter = counter;
     A.polar_jacobi = E.polar_jacobi ? 1 : 0;
+    A.polar_mma = getenv("QF_POLAR_MMA") ? atoi(getenv("QF_POLAR_MMA")) : 1;
+    A.serial_smsp = getenv("QF_SERIAL_SMSP") ? atoi(getenv("QF_SERIAL_SMSP")) : 0;
+    A.sw_ilp = getenv("QF_SW_ILP") ? atoi(getenv("QF_SW_ILP")) : 1;
     A.gather_ltpo_max = getenv("QF_GATHER_LTPO") ? std::max(0, std::min(5, atoi(getenv("QF_GATHER_LTPO")))) : 5;
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;
@@ -1288,10 +1357,10 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.rec_cost = reinterpret_cast<double *>(W + E.L.rec_cost);
     A.rec_gates = reinterpret_cast<double *>(W + E.L.rec_gates);
     A.var_doubles = c.var_doubles;
-    const int threads = resident_threads(c.n);
-    const size_t smem = (size_t)N * N * 16 + 8 * 64 * 16;
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
+    const int threads = resident_threads(c.n, maxm);
+    const size_t smem = resident_smem(N, resident_wide(c.n, maxm));
     auto kern = resident_kernel(c.n, maxm);
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -1608,8 +1677,9 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
     return at;
   };
   struct Off {
-    size_t tgt, vdag, cm, gd, gates, gtab;
+    size_t tgt, vdag, cm, gd, gates, gtab, wdt;
     std::vector<GateDesc> desc;
+    std::vector<WDesc> wd;
     std::vector<int2> tab;
   };
   std::vector<Off> off(np);
@@ -1624,6 +1694,8 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
     off[q].vdag = take(N * N * 16);
     off[q].cm = take(c.const_mats.size() * 8);
     off[q].gd = take(off[q].desc.size() * sizeof(GateDesc));
+    off[q].wd = make_wdescs(off[q].desc);
+    off[q].wdt = take(off[q].wd.size() * sizeof(WDesc));
     off[q].gates = take((size_t)S[q] * c.var_doubles * 8);
     off[q].gtab = take(off[q].tab.size() * sizeof(int2));
   }
@@ -1663,6 +1735,9 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
       QF_CHECK(cudaMemcpyAsync(W + off[q].cm, c.const_mats.data(), c.const_mats.size() * 8,
                                cudaMemcpyHostToDevice, st));
     if (!off[q].desc.empty())
+      QF_CHECK(cudaMemcpyAsync(W + off[q].wdt, off[q].wd.data(), off[q].wd.size() * sizeof(WDesc),
+                               cudaMemcpyHostToDevice, st));
+    if (!off[q].desc.empty())
       QF_CHECK(cudaMemcpyAsync(W + off[q].gd, off[q].desc.data(),
                                off[q].desc.size() * sizeof(GateDesc), cudaMemcpyHostToDevice, st));
     if (!off[q].tab.empty())
@@ -1694,6 +1769,7 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
     P.var_doubles = c.var_doubles;
     P.gstride = c.var_doubles / 2;
     P.gd = reinterpret_cast<const GateDesc *>(W + off[q].gd);
+    P.wdt = reinterpret_cast<const WDesc *>(W + off[q].wdt);
     P.vdag = reinterpret_cast<const double2 *>(W + off[q].vdag);
     P.cmats = reinterpret_cast<const double2 *>(W + off[q].cm);
     P.gates = reinterpret_cast<double2 *>(W + off[q].gates);
@@ -1722,6 +1798,7 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
   A.nprob = np;
   A.counter = counter;
   A.polar_jacobi = 0;
+  A.polar_mma = getenv("QF_POLAR_MMA") ? atoi(getenv("QF_POLAR_MMA")) : 1;
   A.gather_ltpo_max = 5;
   A.dist_tol = p.dist_tol;
   A.diff_tol_a = p.diff_tol_a;
@@ -1738,13 +1815,19 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
   A.iters = reinterpret_cast<int *>(W + o_iters);
   A.verdict = reinterpret_cast<int *>(W + o_verdict);
   A.R = 0;
-  const int threads = resident_threads(maxn);
-  const size_t smem = (size_t)A.N * A.N * 16 + 8 * 64 * 16;
+  // the WIDE variant when every problem qualifies (n >= 5, gates <= 2 qubits),
+  // so a problem's results match its single-problem call bitwise
+  int minn = maxn;
+  for (int q = 0; q < np; q++) minn = std::min(minn, cs[q]->n);
+  const bool wide = resident_wide(minn, maxm) && resident_wide(maxn, maxm);
+  const int threads = wide ? 256 : resident_threads(maxn);
+  const size_t smem = resident_smem(A.N, wide);
   const bool small = maxn <= 4;
-  auto kern = small ? (maxm == 1 ? k_resident<2, true, true> : maxm == 2 ? k_resident<4, true, true>
-                                                                         : k_resident<8, true, true>)
-                    : (maxm == 1 ? k_resident<2, true> : maxm == 2 ? k_resident<4, true>
-                                                                   : k_resident<8, true>);
+  auto kern = wide ? k_resident<4, true, false, true>
+              : small ? (maxm == 1 ? k_resident<2, true, true> : maxm == 2 ? k_resident<4, true, true>
+                                                                           : k_resident<8, true, true>)
+                      : (maxm == 1 ? k_resident<2, true> : maxm == 2 ? k_resident<4, true>
+                                                                     : k_resident<8, true>);
   QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
@@ -1875,6 +1958,7 @@ extern "C" void qf_debug_polar_counts(unsigned long long *out) {
   cudaMemcpyFromSymbol(&out[7], qf::qf_t_form, 8);
   cudaMemcpyFromSymbol(&out[8], qf::qf_t_polar, 8);
   cudaMemcpyFromSymbol(&out[9], qf::qf_n_upd, 8);
+  cudaMemcpyFromSymbol(&out[10], qf::qf_t_ovl, 32);
 }
 // row-tile d = 8 phase timers: wait-for-data, phase 1, phase 2, epilogue, tiles
 extern "C" void qf_debug_rows_counts(unsigned long long *out) {

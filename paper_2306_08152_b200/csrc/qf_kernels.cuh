@@ -673,6 +673,122 @@ __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U,
   return done;
 }
 
+// The same quintic Newton-Schulz polar factor for D = 4 on the FP64 tensor
+// path: complex 4 x 4 products as real 8 x 8 ones through the embedding
+// E(X) = [[Re X, -Im X], [Im X, Re X]] (E(X^H) = E(X)^T, E(XY) = E(X)E(Y)),
+// two mma.m8n8k4 per product.  A lane keeps X as its "column fragment"
+// E(X)[4h + l%4][l/4] (= both operands of X^T X) and "row fragment"
+// E(X)[l/4][4h + l%4] (operand A of X W); Y and W are symmetric, so one row
+// fragment serves as both operands of Y Y and as operand B of X W.  Fragments
+// are re-formed from the MMA accumulator layout E[l/4][2(l%4) + i] by
+// shuffles.  The scaling, the step rule (steep quintic while some |Y - I|
+// entry > 0.55, at most 8 steps; stop one step after max |Y - I| <= 1e-5;
+// hand a singular A to Jacobi after 16 steps) and the convergence tests are
+// those of warp_polar_ns; only the association of the sums differs.  Six MMAs
+// per step on one warp instead of ~150 dependent DFMAs: the serial chain of
+// the resident engine's overlapped step competes with the sandwich's MMAs for
+// the one FP64 pipe, and few long instructions lose less to that contention.
+// Am: A (4 x 4, row-major); U: result (may alias Am).  Returns false as
+// warp_polar_ns does, with the current iterate in Am (same polar factor).
+__device__ __forceinline__ double emb4(const double2 *M, int r, int c) {
+  const double2 v = M[(r & 3) * 4 + (c & 3)];
+  return (r >> 2) == (c >> 2) ? v.x : ((r >> 2) ? v.y : -v.y);
+}
+// row fragment h of a symmetric-or-not 8 x 8 matrix held in accumulator layout
+__device__ __forceinline__ double mma_rowfrag(double c0, double c1, int h, int lane) {
+  const int src = (lane & ~3) | (2 * h + ((lane & 3) >> 1));
+  const double v0 = __shfl_sync(0xffffffffu, c0, src), v1 = __shfl_sync(0xffffffffu, c1, src);
+  return (lane & 1) ? v1 : v0;
+}
+__device__ __forceinline__ double mma_colfrag(double c0, double c1, int h, int lane) {
+  const int src = ((4 * h + (lane & 3)) << 2) | ((lane >> 2) >> 1);
+  const double v0 = __shfl_sync(0xffffffffu, c0, src), v1 = __shfl_sync(0xffffffffu, c1, src);
+  return ((lane >> 2) & 1) ? v1 : v0;
+}
+
+__device__ bool warp_polar_ns_mma4(double2 *Am, double2 *U, int lane) {
+  const int m = lane >> 2, q = lane & 3;
+  double xc[2], xr[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    xc[h] = emb4(Am, 4 * h + q, m);
+    xr[h] = emb4(Am, m, 4 * h + q);
+  }
+  double x0 = 0.0, x1 = 0.0;  // the iterate in accumulator layout (after a step)
+  bool done = false, fast = true;
+  int it = 0;
+#ifdef QF_POLAR_COUNT
+  if (lane == 0) atomicAdd(&qf_ns_calls, 1ull);
+#endif
+  for (; it < 48 && !done; it++) {
+#ifdef QF_POLAR_COUNT
+    if (lane == 0) atomicAdd(&qf_ns_iters, 1ull);
+#endif
+    double y0 = 0.0, y1 = 0.0;  // Y = X^T X
+    ptx::dmma(y0, y1, xc[0], xc[0]);
+    ptx::dmma(y0, y1, xc[1], xc[1]);
+    if (it == 0) {  // X_0 = A / sqrt(g), g >= sigma_max^2 (largest absolute row sum of Y)
+      double rs = fabs(y0) + fabs(y1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(__double_as_longlong(rs) >> 32));
+      if (hi == 0u || hi >= 0x7ff00000u) return false;  // A = 0, or Inf / NaN entries (Am intact)
+      const double gmax = __longlong_as_double((long long)(hi + 1u) << 32);
+      const double s1 = rsqrt(gmax * (1.0 + 1e-5)), s2 = s1 * s1;
+      xc[0] *= s1;
+      xc[1] *= s1;
+      xr[0] *= s1;
+      xr[1] *= s1;
+      y0 *= s2;
+      y1 *= s2;
+    }
+    // 2 = some |Y - I| entry > 0.55 (or NaN), 1 = some > 1e-5, 0 = converged
+    unsigned code = 0;
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      const double a = fabs((i ? y1 : y0) - (m == 2 * q + i ? 1.0 : 0.0));
+      const unsigned ci = !(a <= 0.55) ? 2u : (!(a <= 1e-5) ? 1u : 0u);
+      code = ci > code ? ci : code;
+    }
+    code = __reduce_max_sync(0xffffffffu, code);
+    if (code == 2u && it >= 16) break;  // singular or nearly so: Jacobi (see warp_polar_ns)
+    done = code == 0;
+    if (fast) fast = it < 8 && code == 2;
+    const double ca = fast ? 3.4445 : 1.875, cb = fast ? -4.7750 : -1.25,
+                 cc = fast ? 2.0315 : 0.375;
+    const double yf0 = mma_rowfrag(y0, y1, 0, lane), yf1 = mma_rowfrag(y0, y1, 1, lane);
+    double z0 = 0.0, z1 = 0.0;  // Y^2
+    ptx::dmma(z0, z1, yf0, yf0);
+    ptx::dmma(z0, z1, yf1, yf1);
+    const double w0 = fma(cc, z0, fma(cb, y0, m == 2 * q ? ca : 0.0));
+    const double w1 = fma(cc, z1, fma(cb, y1, m == 2 * q + 1 ? ca : 0.0));
+    const double wf0 = mma_rowfrag(w0, w1, 0, lane), wf1 = mma_rowfrag(w0, w1, 1, lane);
+    x0 = x1 = 0.0;  // X <- X W
+    ptx::dmma(x0, x1, xr[0], wf0);
+    ptx::dmma(x0, x1, xr[1], wf1);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      xr[h] = mma_rowfrag(x0, x1, h, lane);
+      xc[h] = mma_colfrag(x0, x1, h, lane);
+    }
+  }
+  // the complex iterate from rows 0..3 of E(X): columns 0..3 Re, 4..7 -Im
+  double2 *dst = done ? U : Am;
+  __syncwarp();
+  if (lane < 16) {
+    double *d = reinterpret_cast<double *>(dst);
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+      const int col = 2 * q + i;
+      const double v = i ? x1 : x0;
+      if (col < 4) d[2 * (m * 4 + col)] = v;
+      else d[2 * (m * 4 + col - 4) + 1] = -v;
+    }
+  }
+  __syncwarp();
+  return done;
+}
+
 // R_z(theta) = diag(1, e^{i theta}) update (reading R19): with
 // A = M^dagger (M = (1 - beta) E + beta u_old^dagger, as formed for the polar
 // factor), Re Tr(M R_z) is maximal at e^{i theta} = A_11 / |A_11|; A_11 = 0
@@ -695,12 +811,14 @@ __device__ __forceinline__ void warp_rz_update(const double2 *Am, const double2 
 // is supplied.  Am, Vm are scratch; the result goes to U.
 template <int D>
 __device__ void warp_polar(double2 *Am, double2 *Vm, double2 *U, int lane,
-                           const double2 *v0 = nullptr, bool jacobi = false) {
+                           const double2 *v0 = nullptr, bool jacobi = false, bool mma = false) {
   if constexpr (D == 2) {
     warp_polar_jacobi<D>(Am, Vm, U, lane, nullptr);
   } else {
     if (jacobi || v0 != nullptr) {
       warp_polar_jacobi<D>(Am, Vm, U, lane, v0);
+    } else if (D == 4 && mma) {
+      if (!warp_polar_ns_mma4(Am, U, lane)) warp_polar_jacobi<D>(Am, Vm, U, lane, nullptr);
     } else if (!warp_polar_ns<D>(Am, Vm, U, U, lane)) {
       warp_polar_jacobi<D>(Am, Vm, U, lane, nullptr);
     }

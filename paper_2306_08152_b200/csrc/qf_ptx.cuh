@@ -97,5 +97,14 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
       : "d"(a), "d"(b));
 }
 
+// The same MMA as an ordered (volatile) statement: ptxas keeps volatile asm in
+// program order, so a caller can interleave independent MMAs between the two
+// halves of a dependent pair (in-order issue; a dependent MMA waits ~26 cycles).
+__device__ __forceinline__ void dmma_o(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 }  // namespace ptx
 }  // namespace qf

@@ -20,6 +20,7 @@ namespace qf {
 #ifdef QF_POLAR_COUNT
 __device__ unsigned long long qf_t_serial, qf_t_sandwich, qf_n_steps;
 __device__ unsigned long long qf_t_gather, qf_t_form, qf_t_polar, qf_n_upd;
+__device__ unsigned long long qf_t_ovl[4];  // WIDE phase A on warp 0: env, staged, prepare; steps
 #endif
 
 struct GateDesc {
@@ -27,6 +28,7 @@ struct GateDesc {
                           // packed gates (VARIABLE, RZ) or in cmats (CONSTANT)
   int mask;               // basis bits of the location
   int voff;               // complex offset of the backward warm-start slot in vstore
+  int pbit;               // d = 4: rest-index bit pairing two column rests per MMA tile
   int abits[8];
   int rest_pos[kMaxQubits];
 };
@@ -34,6 +36,11 @@ struct GateDesc {
 // the gate table travels in the kernel parameters (constant bank: uniform,
 // cached loads); templates with more gates use the streaming engine
 constexpr int kResMaxGates = 240;
+#ifndef QF_RES_DMMA4
+#define QF_RES_DMMA4 1
+#endif
+constexpr bool kResDmma4 = QF_RES_DMMA4 != 0;  // d = 4 sandwich on the FP64 MMA path (n >= 5)
+constexpr int kResTabBytes = 2 * 128 * 4;  // shared memory for two MMA tile tables (n <= 6)
 
 // One problem of a multi-problem launch (NEXT-2, qf_instantiate_many): its
 // starts are [start0, start0 + S) of the launch's global start numbering;
@@ -45,6 +52,7 @@ struct ResProb {
   const double2 *vdag;   // N x N
   const double2 *cmats;  // CONSTANT gate matrices
   double2 *gates;        // S x gstride: packed VARIABLE gates
+  const struct WDesc *wdt;  // WIDE: 2p transitions (host-built)
 };
 
 // What a CTA needs of the problem of the start it runs (uniform values)
@@ -52,6 +60,7 @@ struct ResView {
   int n, N, p;
   const double2 *vdag, *cmats;
   double2 *u0;  // this start's packed gates
+  const struct WDesc *wdt;  // WIDE: the problem's transition table
 };
 
 struct ResidentArgs {
@@ -67,6 +76,10 @@ struct ResidentArgs {
   const ResProb *probs;  // multi-problem launch: nprob problems, S = sum of starts
   int nprob;
   int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
+  int polar_mma;      // 1: 4 x 4 Newton-Schulz on the FP64 MMA path (warp_polar_ns_mma4)
+  const struct WDesc *wdt;  // WIDE: transitions j -> j + 1 of one sweep (2p, host-built)
+  int serial_smsp;    // WIDE: warp 4 (warp 0's sub-partition) idles in the overlapped phase
+  int sw_ilp;         // WIDE: MMA tiles in flight per sandwich warp while warp 0 prepares
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
   // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
@@ -88,15 +101,28 @@ struct ResidentArgs {
 };
 
 // Shared-memory layout of the resident tensor: element (i, j) at
-// i*N + swz(j), swz(j) = j ^ f(j >> 3 & 7) -- a bijection within each row that
-// spreads the strided column sets of low-bit gates over the 8 bank groups of
-// a 128-byte wavefront (f searched over all 1-3-qubit locations at n <= 6 for
-// the block thread mapping: 392 vs 840 wavefronts unswizzled at n = 6,
-// worst case 2-way instead of 8-way).
-__device__ __forceinline__ int swz(int j) {
-  return j ^ (int)((0x41362750u >> (4 * ((j >> 3) & 7))) & 7u);
+// i*N + (j ^ F(i, j)), F(i, j) = fr(i) ^ fc(j >> 3) restricted to the low three
+// column bits (and to N - 1 below N = 8) -- a bijection within each row.  fr
+// and fc are GF(2)-linear: row basis bit p contributes kSwRow[p], column bit
+// 3 + p contributes kSwCol[p] (three-bit values).  A 128-byte shared-memory
+// wavefront holds 8 double2, so a quarter-warp's 8 accesses are conflict-free
+// iff their three difference bits map to independent bank vectors.  The values
+// were searched (GF(2) ranks over every ordered 2-qubit location at n = 5, 6)
+// for the two access patterns of the FP64-MMA block sandwich
+// (res_sandwich_dmma4): loads differ in the gate's two row bits and a column
+// "pairing" bit w, stores in the gate's MSB row bit, its LSB column bit and w;
+// the host picks w per gate (pick_pair_bit) so both sets are independent.
+constexpr int kSwRow[6] = {1, 2, 3, 5, 6, 7};
+constexpr int kSwCol[3] = {5, 6, 4};
+// the same maps as nibble tables over three bits at a time
+constexpr unsigned kSwRowLo = 0x01233210u;  // row bits 0..2 -> XOR of {1, 2, 3}
+constexpr unsigned kSwRowHi = 0x41273650u;  // row bits 3..5 -> XOR of {5, 6, 7}
+constexpr unsigned kSwColT = 0x72143650u;   // column bits 3..5 -> XOR of {5, 6, 4}
+__host__ __device__ __forceinline__ int sidx(int i, int j, int N) {
+  const unsigned f = (kSwRowLo >> (4 * (i & 7))) ^ (kSwRowHi >> (4 * ((i >> 3) & 7))) ^
+                     (kSwColT >> (4 * ((j >> 3) & 7)));
+  return i * N + (j ^ (int)(f & (unsigned)(N - 1) & 7u));
 }
-__device__ __forceinline__ int sidx(int i, int j, int N) { return i * N + swz(j); }
 
 __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
   return insert_zeros(r, g.mask);
@@ -147,6 +173,123 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
   }
 }
 
+// ct <- E(L) ct E(R) in place for a 4 x 4 gate on the FP64 tensor path
+// (mma.sync m8n8k4 f64, the same FP64 pipe as DFMA but 256 FMAs per issued
+// instruction, so a warp keeps the pipe busy with few registers and issue
+// slots).  Complex products as real ones through the embedding
+// emb(M) = [[Re M, -Im M], [Im M, Re M]].  One warp-tile = row rest r and two
+// column rests c0, c1 = c0 | bit pbit (8 columns):
+//   stage 1  Y = L X:      emb(L) (8 x 8) [Re X; Im X] (8 x 8 columns), two MMAs
+//            (k = the four rows ins(k, r), re then im);
+//   stage 2  Z^T = R^T Y^T: emb(R^T) [Re Y^T; Im Y^T], two MMAs, N = (row a,
+//            column rest c).
+// With stage 1's columns ordered n = 2 kc + csel, the lane holding stage 1's
+// outputs (Re or Im) Y[a][ins(kc, c_i)], i = 0, 1, needs for stage 2's B
+// operand one of them and one from lane ^ 16 (one 64-bit shuffle), and stage
+// 2's outputs are re-paired (Re, Im) by one more shuffle, so each element
+// costs one 16-byte shared-memory load and one store (different lanes, same
+// tile: in place).  The swizzle (sidx) makes both conflict-free.  Tiles are
+// spread over warps w0, w0 + nw, ...; two in flight per warp.
+// x with zero bits inserted at basis positions p0 < p1 (the rest index of a
+// 2-qubit location spread over the other basis bits), branch-free
+__host__ __device__ __forceinline__ int insert2(int x, int p0, int p1) {
+  x = ((x >> p0) << (p0 + 1)) | (x & ((1 << p0) - 1));
+  return ((x >> p1) << (p1 + 1)) | (x & ((1 << p1) - 1));
+}
+
+// The swizzled address is GF(2)-linear in the basis bits of (row, column):
+// sidx(i, j) = (i << n) ^ j ^ F(i, j).  So a tile element's address is the
+// XOR of a per-tile part (row rest, column rests) and a per-lane part (local
+// row / column, which of the two column rests).  res_dmma4_table writes the
+// per-tile parts of gate g for all tiles (all threads, before the barrier that
+// precedes the sandwich); the tile loop then costs one broadcast load and two
+// XORs of index arithmetic per tile.
+__device__ __forceinline__ int res_dmma4_tiles(int n) { return 1 << (2 * n - 5); }
+
+__device__ __forceinline__ void res_dmma4_table(const GateDesc &g, int n, int N, int *tab) {
+  const int lhalf = n - 3, ntile = res_dmma4_tiles(n);
+  const int p0 = __ffs(g.mask) - 1, p1 = 31 - __clz(g.mask);
+  const int pb = g.pbit, pmask = (1 << pb) - 1;
+  for (int t = threadIdx.x; t < ntile; t += blockDim.x) {
+    const int cp = t & ((1 << lhalf) - 1);
+    const int c0 = ((cp & ~pmask) << 1) | (cp & pmask);
+    tab[t] = sidx(insert2(t >> lhalf, p0, p1), insert2(c0, p0, p1), N);
+  }
+}
+
+template <int ILP = 4, bool SPLIT = false>
+__device__ __forceinline__ void res_sandwich_dmma4(double2 *ct, const GateDesc &g, int n, int N,
+                                                   const double2 *Ls, const double2 *Rs,
+                                                   const int *tab, int w0, int nw) {
+  const int lane = threadIdx.x & 31;
+  const int ntile = res_dmma4_tiles(n);
+  const int m = lane >> 2, kq = lane & 3;
+  // A operands: emb(L) columns (re part k, im part k) and emb(R^T) likewise
+  const double2 l = Ls[(m & 3) * 4 + kq];
+  const double a1 = m < 4 ? l.x : l.y, a2 = m < 4 ? -l.y : l.x;
+  const double2 rr = Rs[kq * 4 + (m & 3)];
+  const double b1 = m < 4 ? rr.x : rr.y, b2 = m < 4 ? -rr.y : rr.x;
+  const int p0 = __ffs(g.mask) - 1, p1 = 31 - __clz(g.mask);
+  const int wbit = insert2(1 << g.pbit, p0, p1);  // basis column bit pairing c0, c1
+  // per-lane parts: load element row ins(kq, r), column ins(kc, c_sel); store
+  // element (after the re/im re-pairing) row ins(a, r), column ins(b, c_sel)
+  const int ld_lane = sidx(g.abits[kq], g.abits[lane >> 3] | (((lane >> 2) & 1) ? wbit : 0), N);
+  const int st_lane = sidx(g.abits[2 * (lane & 1) + (lane >> 4)],
+                           g.abits[(lane >> 2) & 3] | (((lane >> 1) & 1) ? wbit : 0), N);
+  const bool lo = lane < 16;
+  for (int t0 = w0; t0 < ntile; t0 += ILP * nw) {
+    double2 x[ILP];
+    int at[ILP];
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      const int t = t0 + u * nw;
+      at[u] = tab[t < ntile ? t : t0];  // idle slots redo tile t0 (not stored)
+      x[u] = ct[at[u] ^ ld_lane];
+    }
+    // issue order matters (in-order issue, 26-cycle MMA latency): the first
+    // MMA of every tile, then the second (accumulating) one of every tile
+    double y[ILP][2], z[ILP][2], bre[ILP], bim[ILP];
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      y[u][0] = y[u][1] = 0.0;
+      ptx::dmma_o(y[u][0], y[u][1], a1, x[u].x);
+      if (SPLIT) {
+        double q0 = 0.0, q1 = 0.0;
+        ptx::dmma_o(q0, q1, a2, x[u].y);
+        y[u][0] += q0;
+        y[u][1] += q1;
+      } else {
+        ptx::dmma_o(y[u][0], y[u][1], a2, x[u].y);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      const double recv = __shfl_xor_sync(0xffffffffu, lo ? y[u][1] : y[u][0], 16);
+      bre[u] = lo ? y[u][0] : recv;
+      bim[u] = lo ? recv : y[u][1];
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      z[u][0] = z[u][1] = 0.0;
+      ptx::dmma_o(z[u][0], z[u][1], b1, bre[u]);
+      if (SPLIT) {
+        double q0 = 0.0, q1 = 0.0;
+        ptx::dmma_o(q0, q1, b2, bim[u]);
+        z[u][0] += q0;
+        z[u][1] += q1;
+      } else {
+        ptx::dmma_o(z[u][0], z[u][1], b2, bim[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; u++) {
+      const double recv = __shfl_xor_sync(0xffffffffu, lo ? z[u][1] : z[u][0], 16);
+      if (t0 + u * nw < ntile)
+        ct[at[u] ^ st_lane] = lo ? make_double2(z[u][0], recv) : make_double2(recv, z[u][1]);
+    }
+  }
+}
+
 // ct <- E(L) ct E(R) in place (R == nullptr: one-sided), all threads.
 template <int D>
 __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const double2 *Ls,
@@ -178,16 +321,15 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
   for (int it = threadIdx.x; it < N * NR; it += nt) {
     const int i = it >> lnr, c = it & (NR - 1);
     const int cb = rspread(g, n, c);
-    double2 *row = ct + i * N;
     double2 z[D];
 #pragma unroll
-    for (int b = 0; b < D; b++) z[b] = row[swz(cb | g.abits[b])];
+    for (int b = 0; b < D; b++) z[b] = ct[sidx(i, cb | g.abits[b], N)];
 #pragma unroll
     for (int b = 0; b < D; b++) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < D; k++) acc = cfma(z[k], Rs[k * D + b], acc);
-      row[swz(cb | g.abits[b])] = acc;
+      ct[sidx(i, cb | g.abits[b], N)] = acc;
     }
   }
   __syncthreads();
@@ -287,7 +429,8 @@ __device__ void res_update(const ResidentArgs &A, const GateDesc &g, double2 *u,
   if (D == 2 && g.kind == 2)
     warp_rz_update(Am, Uo, Pm, lane);  // R_z gate: analytic update
   else
-    warp_polar<D>(Am, Vm, Pm, lane, vs ? Vm : nullptr, A.polar_jacobi != 0);  // u_new -> Pm
+    warp_polar<D>(Am, Vm, Pm, lane, vs ? Vm : nullptr, A.polar_jacobi != 0,
+                  A.polar_mma != 0);  // u_new -> Pm
 #ifdef QF_POLAR_COUNT
   if (lane == 0) {
     const long long q3 = clock64();
@@ -354,9 +497,18 @@ __device__ __forceinline__ void res_prepare(const ResidentArgs &A, const ResView
 // when there are at least as many d x d blocks as threads; otherwise (small n:
 // e.g. 4 blocks for a 4 x 4 gate at n = 3) the two-phase form, whose column /
 // row items keep every lane busy (fewer, shorter dependent chains), as for d = 8.
-template <int MAXD, bool SMALL = false>
+// the FP64-MMA d = 4 sandwich runs in the WIDE variant only: in the 128-thread
+// kernel (one warp per sub-partition per CTA) it measured slower than the
+// register blocks (C4, 40 sweeps: 459 vs 439 ms)
+template <int MAXD, bool SMALL = false, bool WIDE = false>
+__device__ __forceinline__ bool res_use_dmma4(const GateDesc &g, const ResView &V) {
+  return WIDE && kResDmma4 && MAXD >= 4 && g.d == 4 && V.n >= 5;
+}
+
+template <int MAXD, bool SMALL = false, bool WIDE = false>
 __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResView &V,
-                                          const double2 *Lb, const double2 *Rb, int t0, int nt) {
+                                          const double2 *Lb, const double2 *Rb, const int *tab,
+                                          int t0, int nt, int ilp = 4) {
   const int nb = V.N / g.d;
   const bool blocks = !SMALL && nb * nb >= nt;
   if (g.d == 2) {
@@ -364,7 +516,12 @@ __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const 
     else res_sandwich<2>(ct, g, V.n, V.N, Lb, Rb);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      if (blocks) res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+      if (WIDE || res_use_dmma4<MAXD, SMALL, WIDE>(g, V)) {
+        if (WIDE && ilp == 1) res_sandwich_dmma4<1>(ct, g, V.n, V.N, Lb, Rb, tab, t0 >> 5, nt >> 5);
+        else if (WIDE && ilp == 2) res_sandwich_dmma4<2>(ct, g, V.n, V.N, Lb, Rb, tab, t0 >> 5, nt >> 5);
+        else res_sandwich_dmma4(ct, g, V.n, V.N, Lb, Rb, tab, t0 >> 5, nt >> 5);
+      }
+      else if (blocks) res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
       else res_sandwich<4>(ct, g, V.n, V.N, Lb, Rb);
     } else if constexpr (MAXD >= 8) {
       res_sandwich<8>(ct, g, V.n, V.N, Lb, Rb);
@@ -414,7 +571,191 @@ __device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
   }
 }
 
-// rest-index bits (of gate g) that belong to the location `next_mask`
+// ------------------------------------------------------------------ overlapped steps (WIDE)
+// The environment of the next step can be formed without waiting for this
+// step's sandwich (SURVEY Sec. 9 note 3; the NEXT-3 identity): with W the
+// qubits of this gate G and the next one G', partial traces over qubits
+// outside W commute with operators on W, so
+//   PT_{not G'}(E(L) ct E(R)) = PT_{W \ G'}(E_W(L) T E_W(R)),
+//   T = PT_{not W}(ct)   (2^|W| x 2^|W|, gathered BEFORE this step's sandwich).
+// Warp 0 computes it from T and runs the next polar factor while the other
+// warps apply this step's sandwich; only the small T gather stays between
+// sandwiches.  Same steps in the same order (exact algebra; only the
+// association of the sums differs).
+
+// bits of x deposited on the set bits of mask (ascending) / the inverse
+__host__ __device__ __forceinline__ int lowbit_pos(int m) {
+#ifdef __CUDA_ARCH__
+  return __ffs(m) - 1;
+#else
+  return __builtin_ctz((unsigned)m);
+#endif
+}
+__host__ __device__ __forceinline__ int popc(int m) {
+#ifdef __CUDA_ARCH__
+  return __popc(m);
+#else
+  return __builtin_popcount((unsigned)m);
+#endif
+}
+__host__ __device__ __forceinline__ int deposit(int x, int mask) {
+  int out = 0;
+  for (int t = 0; mask; t++) {
+    const int p = lowbit_pos(mask);
+    mask &= mask - 1;
+    out |= ((x >> t) & 1) << p;
+  }
+  return out;
+}
+__host__ __device__ __forceinline__ int compress(int pat, int mask) {
+  int out = 0;
+  for (int t = 0; mask; t++) {
+    const int p = lowbit_pos(mask);
+    mask &= mask - 1;
+    out |= ((pat >> p) & 1) << t;
+  }
+  return out;
+}
+
+// A transition j -> j + 1 in W space: gate j relocated to the |W|-qubit index
+// space of T (compressed basis bits, pairing bit 0 and the MMA tile bases of
+// the T sandwich), and the next gate's local index patterns and rest
+// patterns for the partial trace.  One table entry per step of a sweep,
+// built on the host (make_wdescs) and prefetched by warp 0 a step ahead.
+struct WDesc {
+  GateDesc gw;
+  int w, d2, S2;
+  int ab2[4];
+  int sb2[8];
+  int tabT[8];
+  int pad[2];
+};
+static_assert(sizeof(WDesc) % 16 == 0 && sizeof(WDesc) <= 32 * 16, "WDesc: whole double2 per lane");
+
+__host__ __device__ inline void res_make_wdesc(const GateDesc &g, const GateDesc &g2, WDesc &D) {
+  const int Wm = g.mask | g2.mask, w = popc(Wm), Wn = 1 << w;
+  D = WDesc{};
+  D.w = w;
+  GateDesc &G = D.gw;
+  G.m = g.m;
+  G.d = g.d;
+  G.kind = g.kind;
+  G.mask = compress(g.mask, Wm);
+  for (int a = 0; a < 8; a++) G.abits[a] = a < g.d ? compress(g.abits[a], Wm) : 0;
+  G.pbit = 0;
+  D.d2 = g2.d;
+  for (int a = 0; a < 4; a++) D.ab2[a] = a < g2.d ? compress(g2.abits[a], Wm) : 0;
+  const int rest2 = (Wn - 1) & ~compress(g2.mask, Wm);
+  D.S2 = Wn / g2.d;
+  for (int q = 0; q < D.S2 && q < 8; q++) D.sb2[q] = deposit(q, rest2);
+  if (g.d == 4 && w >= 3) {  // tile bases of the T sandwich (res_dmma4_table, n = w)
+    const int lhalf = w - 3, ntile = 1 << (2 * w - 5);
+    int p0 = lowbit_pos(G.mask), p1 = p0;
+    for (int b = 0; b < 31; b++)
+      if ((G.mask >> b) & 1) p1 = b;
+    for (int t = 0; t < ntile && t < 8; t++)
+      D.tabT[t] = sidx(insert2(t >> lhalf, p0, p1),  // column pair (c0, c0 | 1): pbit 0
+                       insert2((t & ((1 << lhalf) - 1)) << 1, p0, p1), Wn);
+  }
+}
+
+// All threads: T[x][y] = sum_r ct[dep(x) | dep(r)][dep(y) | dep(r)] over the
+// rest r of the qubit set W (basis mask Wm), |W| <= 4, into Tm in the swizzled
+// layout of a |W|-qubit tensor (sidx(x, y, 2^|W|)).  TPO threads of a warp per
+// output take r = k, k + TPO, ... ascending, then a fixed xor tree.  Element
+// addresses are XORs of an output part and per-rest-bit parts (sidx is
+// GF(2)-linear), so the term loop does no index arithmetic.
+__device__ void res_gather_T(const ResView &V, const double2 *ct, int Wm, double2 *Tm) {
+  const int w = __popc(Wm), Wn = 1 << w, O = Wn * Wn, nt = blockDim.x;
+  const int rmask = (V.N - 1) & ~Wm, R = V.N >> w;
+  int ltpo = (31 - __clz(nt)) - 2 * w;
+  ltpo = ltpo < 0 ? 0 : (ltpo > 5 ? 5 : ltpo);
+  ltpo = ltpo > V.n - w ? V.n - w : ltpo;
+  const int tpo = 1 << ltpo, groups = nt >> ltpo, k = threadIdx.x & (tpo - 1);
+  int rb[4];
+#pragma unroll
+  for (int t = 0; t < 4; t++) {
+    const int bit = deposit(1 << t, rmask);
+    rb[t] = bit ? sidx(bit, bit, V.N) : 0;
+  }
+  for (int o0 = threadIdx.x >> ltpo; o0 < O + groups - 1; o0 += groups) {
+    double2 acc = make_double2(0.0, 0.0);
+    if (o0 < O) {
+      const int base = sidx(deposit(o0 >> w, Wm), deposit(o0 & (Wn - 1), Wm), V.N);
+      for (int r = k; r < R; r += tpo) {
+        int a = base;
+#pragma unroll
+        for (int t = 0; t < 4; t++) a ^= ((r >> t) & 1) ? rb[t] : 0;
+        const double2 v = ct[a];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+    }
+    for (int off = 1; off < tpo; off <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (k == 0 && o0 < O) Tm[sidx(o0 >> w, o0 & (Wn - 1), Wn)] = acc;
+    if (o0 + groups >= O) break;
+  }
+}
+
+// one warp, in place on T (swizzled Wn x Wn): T <- E_W(L) T (left) or
+// T E_W(R) (right) for a D x D gate G (W-space descriptor)
+template <int D, bool RIGHT>
+__device__ __forceinline__ void res_T_apply(double2 *Tm, int w, const GateDesc &G,
+                                            const double2 *M, int lane) {
+  const int Wn = 1 << w, items = Wn * (Wn / D), restm = (Wn - 1) & ~G.mask;
+  for (int it = lane; it < items; it += 32) {
+    const int other = it & (Wn - 1), rb = deposit(it >> w, restm);
+    double2 v[D];
+#pragma unroll
+    for (int k = 0; k < D; k++)
+      v[k] = RIGHT ? Tm[sidx(other, rb | G.abits[k], Wn)] : Tm[sidx(rb | G.abits[k], other, Wn)];
+#pragma unroll
+    for (int a = 0; a < D; a++) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < D; k++) acc = RIGHT ? cfma(v[k], M[k * D + a], acc) : cfma(M[a * D + k], v[k], acc);
+      if (RIGHT) Tm[sidx(other, rb | G.abits[a], Wn)] = acc;
+      else Tm[sidx(rb | G.abits[a], other, Wn)] = acc;
+    }
+  }
+  __syncwarp();
+}
+
+// warp 0: P' = PT_{W \ G'}(E_W(L) T E_W(R)) for the next gate from T (in
+// place) and this step's operands (L, R): a 4 x 4 gate with |W| >= 3 on the
+// FP64 MMA path (the resident sandwich on the |W|-qubit T), else DFMA
+template <int MAXD>
+__device__ void res_env_from_T(double2 *Tm, const WDesc &D, const double2 *L, const double2 *R,
+                               double2 *Pm, int lane) {
+  const int w = D.w, Wn = 1 << w;
+  if (D.gw.d == 2) {
+    res_T_apply<2, false>(Tm, w, D.gw, L, lane);
+    res_T_apply<2, true>(Tm, w, D.gw, R, lane);
+  } else if constexpr (MAXD >= 4) {
+    if (w >= 3) {
+      res_sandwich_dmma4(Tm, D.gw, w, Wn, L, R, D.tabT, 0, 1);
+      __syncwarp();
+    } else {
+      res_T_apply<4, false>(Tm, w, D.gw, L, lane);
+      res_T_apply<4, true>(Tm, w, D.gw, R, lane);
+    }
+  }
+  const int d2 = D.d2, ld2 = d2 == 4 ? 2 : 1;
+  if (lane < d2 * d2) {
+    const int a = lane >> ld2, b = lane & (d2 - 1);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = 0; q < D.S2; q++) {
+      const double2 v = Tm[sidx(D.sb2[q] | D.ab2[a], D.sb2[q] | D.ab2[b], Wn)];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    Pm[lane] = acc;
+  }
+  __syncwarp();
+}
 
 // Grid-wide barrier for a launch whose CTAs are all resident (checked by the
 // host against the occupancy before choosing this path): arrivals count up
@@ -444,16 +785,25 @@ __device__ __forceinline__ void res_grid_barrier(unsigned *gbar, unsigned nblock
 // problem's gate table is read from the kernel parameters.
 // SMALL (every problem n <= 4): the two-phase sandwich only -- no register
 // block path, far fewer registers, more CTAs (starts) per SM.
-template <int MAXD, bool MULTI, bool SMALL = false>
-__global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(const __grid_constant__ ResidentArgs A) {
+// WIDE (n = 5, 6 with gates of at most 2 qubits): 256 threads, <= 80
+// registers -- the FP64-MMA sandwich needs few registers, and two warps per
+// SMSP per CTA keep the MMA pipe busy (tools/sandwich_bench.cu: 94 % of the
+// pipe with 3 CTAs per SM in the sandwich, 54 % with one).
+template <int MAXD, bool MULTI, bool SMALL = false, bool WIDE = false>
+__global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3) k_resident(const __grid_constant__ ResidentArgs A) {
   extern __shared__ __align__(128) unsigned char smraw[];
+  // operand slots of SL complex each (WIDE: d <= 4 -> 16, else 64)
+  constexpr int SL = WIDE ? 16 : 64;
   double2 *ct = reinterpret_cast<double2 *>(smraw);
-  double2 *Lb = ct + A.N * A.N;  // [2][64]; A.N = the largest N of the launch
-  double2 *Rb = Lb + 128;        // [2][64]
-  double2 *Uo = Rb + 128;
-  double2 *Pm = Uo + 64;
-  double2 *Am = Pm + 64;
-  double2 *Vm = Am + 64;
+  double2 *Lb = ct + A.N * A.N;  // [2][SL]; A.N = the largest N of the launch
+  double2 *Rb = Lb + 2 * SL;     // [2][SL]
+  double2 *Uo = Rb + 2 * SL;
+  double2 *Pm = Uo + SL;
+  double2 *Am = Pm + SL;
+  double2 *Vm = Am + SL;
+  int *tabs = reinterpret_cast<int *>(Vm + SL);  // [2][128] d = 4 MMA tile addresses (n <= 6)
+  double2 *Tm = reinterpret_cast<double2 *>(tabs + 256);  // WIDE: T (<= 16 x 16)
+  WDesc *wd = reinterpret_cast<WDesc *>(Tm + 256);        // WIDE: transition in W space
   const GateDesc *gdesc = A.gd;  // kernel parameters (constant bank); MULTI: per problem
   __shared__ int s_start, s_verdict;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -485,6 +835,7 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
       V.vdag = P.vdag;
       V.cmats = P.cmats;
       V.u0 = P.gates + (long long)(s - P.start0) * P.gstride;
+      V.wdt = P.wdt;
       gdesc = P.gd;  // global memory
     } else {
       V.n = A.n;
@@ -493,6 +844,7 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
       V.vdag = A.vdag;
       V.cmats = A.cmats;
       V.u0 = A.gates + (long long)s * A.gstride;
+      V.wdt = A.wdt;
     }
     const int steps = 2 * V.p;
     auto gate_of = [&](int j, int &fw) {
@@ -509,7 +861,9 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
     auto prepare = [&](int j2, bool pre) {
       int fw2;
       const GateDesc &g2 = gdesc[gate_of(j2, fw2)];
-      const int off = (j2 & 1) * 64;
+      const int off = (j2 & 1) * SL;
+      if (res_use_dmma4<MAXD, SMALL, WIDE>(g2, V))
+        res_dmma4_table(g2, V.n, V.N, tabs + (j2 & 1) * 128);  // barriers follow
       if (g2.kind != 1) {
 #ifdef QF_POLAR_COUNT
         const long long tg0 = clock64();
@@ -539,13 +893,119 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
       if (serial) res_prepare<MAXD>(A, V, ct, g2, s, fw2, Lb + off, Rb + off, Uo, Pm, Am, Vm, lane);
       __syncthreads();
     };
-    if (A.max_iters > 0) prepare(0, false);
+    // WIDE: is the environment of step j + 1 formed from T while step j's
+    // sandwich runs (|W| <= 4; a CONSTANT next gate needs no environment)
+    auto ovl_ok = [&](int j) -> bool {
+      if (j + 1 >= steps) return false;
+      int f1, f2;
+      const GateDesc &ga = gdesc[gate_of(j, f1)], &gb = gdesc[gate_of(j + 1, f2)];
+      return gb.kind == 1 || __popc(ga.mask | gb.mask) <= 4;
+    };
+    auto gather_T = [&](int j) {  // all threads, T of transition j -> j + 1
+      int f1, f2;
+      const GateDesc &ga = gdesc[gate_of(j, f1)], &gb = gdesc[gate_of(j + 1, f2)];
+      if (gb.kind != 1) res_gather_T(V, ct, ga.mask | gb.mask, Tm);
+    };
+    // WIDE: warp 0 holds the next transition's W descriptor in registers
+    // (one double2 per lane), loaded a step ahead of its use
+    constexpr int kWdv = sizeof(WDesc) / 16;
+    double2 wpre = make_double2(0.0, 0.0);
+    auto wd_fetch = [&](int j) {
+      if (WIDE && serial && lane < kWdv && j < steps)
+        wpre = reinterpret_cast<const double2 *>(V.wdt + j)[lane];
+    };
+    if (A.max_iters > 0) {
+      prepare(0, false);
+      wd_fetch(0);
+      if constexpr (WIDE) {
+        if (ovl_ok(0)) {
+          gather_T(0);
+          __syncthreads();
+        }
+      }
+    }
     for (;;) {
-      if (A.max_iters > 0) {
+      if (WIDE && A.max_iters > 0) {
         for (int j = 0; j < steps; j++) {
           int fw;
           const GateDesc &g = gdesc[gate_of(j, fw)];
-          const int buf = (j & 1) * 64;
+          const int buf = (j & 1) * SL;
+          const bool has_next = j + 1 < steps, ov = ovl_ok(j);
+#ifdef QF_POLAR_COUNT
+          const long long c0 = clock64();
+#endif
+          if (serial) {  // the W descriptor of transition j -> j + 1, prefetch the next
+            if (ov && lane < kWdv) reinterpret_cast<double2 *>(wd)[lane] = wpre;
+            __syncwarp();
+            wd_fetch(j + 1);
+          }
+          if (ov && serial) {
+            // warp 0: operands of step j + 1 (environment from T, polar factor)
+            int fw2;
+            const GateDesc &g2 = gdesc[gate_of(j + 1, fw2)];
+            const double2 *u2 = (g2.kind != 1 ? V.u0 : V.cmats) + g2.goff;
+            const double2 uo = lane < g2.d * g2.d ? u2[lane] : make_double2(0.0, 0.0);
+            if (g2.kind != 1) res_env_from_T<MAXD>(Tm, *wd, Lb + buf, Rb + buf, Pm, lane);
+#ifdef QF_POLAR_COUNT
+            const long long e1 = clock64();
+#endif
+            if (lane < g2.d * g2.d) Uo[lane] = uo;
+            __syncwarp();
+#ifdef QF_POLAR_COUNT
+            const long long e2 = clock64();
+#endif
+            res_prepare<MAXD>(A, V, ct, g2, s, fw2, Lb + (buf ^ SL), Rb + (buf ^ SL), Uo, Pm, Am,
+                              Vm, lane);
+#ifdef QF_POLAR_COUNT
+            if (lane == 0) {
+              atomicAdd(&qf_t_ovl[0], (unsigned long long)(e1 - c0));
+              atomicAdd(&qf_t_ovl[1], (unsigned long long)(e2 - e1));
+              atomicAdd(&qf_t_ovl[2], (unsigned long long)(clock64() - e2));
+              atomicAdd(&qf_t_ovl[3], 1ull);
+            }
+#endif
+          } else if (!(ov && A.serial_smsp && (tid >> 5) == 4)) {
+            // the sandwich of step j: warps 1.. while warp 0 prepares, else all
+            // (serial_smsp: warp 4, which shares warp 0's SM sub-partition, idles)
+            int t0 = ov ? tid - 32 : tid, ntw = ov ? nt - 32 : nt;
+            if (ov && A.serial_smsp) {
+              t0 = tid - 32 * (tid >= 160 ? 2 : 1);
+              ntw = nt - 64;
+            }
+            res_apply<MAXD, SMALL, WIDE>(ct, g, V, Lb + buf, Rb + buf, tabs + (j & 1) * 128, t0, ntw,
+                                         ov ? A.sw_ilp : 4);
+          }
+#ifdef QF_POLAR_COUNT
+          const long long c1 = clock64();
+          if (tid == 0) atomicAdd(&qf_t_serial, (unsigned long long)(c1 - c0));
+          if (tid == 32) atomicAdd(&qf_t_sandwich, (unsigned long long)(c1 - c0));
+#endif
+          __syncthreads();
+          if (has_next) {
+            if (!ov) {
+              prepare(j + 1, false);
+            } else {
+              int fw2;
+              const GateDesc &g2 = gdesc[gate_of(j + 1, fw2)];
+              if (res_use_dmma4<MAXD, SMALL, WIDE>(g2, V))
+                res_dmma4_table(g2, V.n, V.N, tabs + ((j + 1) & 1) * 128);
+            }
+            if (ovl_ok(j + 1)) gather_T(j + 1);
+            __syncthreads();
+          }
+#ifdef QF_POLAR_COUNT
+          if (tid == 0) {
+            atomicAdd(&qf_t_gather, (unsigned long long)(clock64() - c1));
+            atomicAdd(&qf_n_steps, 1ull);
+          }
+#endif
+        }
+        it++;
+      } else if (A.max_iters > 0) {
+        for (int j = 0; j < steps; j++) {
+          int fw;
+          const GateDesc &g = gdesc[gate_of(j, fw)];
+          const int buf = (j & 1) * SL;
           const bool has_next = j + 1 < steps;
           if (has_next && serial) {  // prefetch u_old of the next gate (L2 latency
             int fw2;                 // hidden behind this sandwich)
@@ -565,7 +1025,7 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
 #ifdef QF_POLAR_COUNT
           const long long c0 = clock64();
 #endif
-          res_apply<MAXD, SMALL>(ct, g, V, Lb + buf, Rb + buf, tid, nt);
+          res_apply<MAXD, SMALL, WIDE>(ct, g, V, Lb + buf, Rb + buf, tabs + (j & 1) * 128, tid, nt);
           __syncthreads();
 #ifdef QF_POLAR_COUNT
           const long long c1 = clock64();
@@ -673,6 +1133,13 @@ __global__ void __launch_bounds__(SMALL ? 64 : 128, SMALL ? 8 : 3) k_resident(co
       }
       if (it % A.reset_iters == 0) res_init<MAXD>(A, V, ct, gdesc, s, Lb);
       prepare(0, false);  // operands of the next sweep's first step
+      wd_fetch(0);
+      if constexpr (WIDE) {
+        if (ovl_ok(0)) {
+          gather_T(0);
+          __syncthreads();
+        }
+      }
     }
     __syncthreads();
   }

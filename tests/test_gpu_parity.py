@@ -143,6 +143,19 @@ def test_parity_random_templates(n, p, seed, engine):
     _compare(gpu, orc, idx, 10, 2 ** n)
 
 
+@pytest.mark.parametrize("n,p,seed", [(5, 12, 11), (6, 10, 12), (5, 24, 3), (6, 30, 4)])
+def test_parity_random_templates_wide(n, p, seed):
+    """Gates of at most 2 qubits at n = 5, 6: the 256-thread resident variant
+    (FP64-MMA sandwich, next environment from T overlapped with the sandwich,
+    MMA Newton-Schulz); 1- and 2-qubit gates, CONSTANT gates, every |W| of
+    consecutive gates, ragged 37 starts, 10 recorded sweeps."""
+    locs, kinds, cm = qfgen.random_template(n, p, arities=(1, 2), seed=seed, const_frac=0.25)
+    V = qfgen.haar(qfgen.stream_key(seed, qfgen.PURPOSE_TARGET, 0, 0), 2 ** n)[0]
+    init = qfgen.initial_gates(n, locs, kinds, 3000 + seed, 0, 37)
+    gpu, orc, idx = _run_pair(n, locs, kinds, cm, V, init, R=10, max_iters=30)
+    _compare(gpu, orc, idx, 10, 2 ** n)
+
+
 def test_parity_n10_tile_kernel():
     """n = 10 takes the register-tile sandwich (rows of 16 KiB are beyond the
     row-tile kernel); 2 starts x 2 sweeps."""

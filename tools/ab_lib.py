@@ -1,7 +1,7 @@
 """A/B timing of library builds / switches on one box:
   python tools/ab_lib.py SPEC_A SPEC_B [SPEC_C ...] [--reps R] [--config C]
 SPEC = path/to/lib.so[@VAR=value[,VAR=value]] (environment for that arm).
-C4 (or `config`), 3 sweeps, resident engine (AB_ENGINE=stream for the
+C4 (or `config`), 3 sweeps (or --sweeps K), resident engine (AB_ENGINE=stream for the
 streaming one); alternates the arms to cancel drift and prints each run's
 wall time of the whole call (ms, best of the last two of three)."""
 import ctypes
@@ -11,10 +11,14 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 args = sys.argv[1:]
-reps, cfg = 3, "C4"
+reps, cfg, sweeps = 3, "C4", 3
 if "--reps" in args:
     i = args.index("--reps")
     reps = int(args[i + 1])
+    del args[i:i + 2]
+if "--sweeps" in args:
+    i = args.index("--sweeps")
+    sweeps = int(args[i + 1])
     del args[i:i + 2]
 if "--config" in args:
     i = args.index("--config")
@@ -33,14 +37,15 @@ dev = torch.device("cuda:0")
 c = qf.Circuit.from_workload(w)
 dV = torch.from_numpy(np.ascontiguousarray(w.target_unitary())).to(dev)
 dI = torch.from_numpy(w.initial()).to(dev)
-ws = torch.empty(qf.qf_workspace_size(c, w.starts, max_iters=3), dtype=torch.uint8, device=dev)
+MI = int(sys.argv[3])
+ws = torch.empty(qf.qf_workspace_size(c, w.starts, max_iters=MI), dtype=torch.uint8, device=dev)
 eng = {"stream": qf.QF_ENGINE_STREAM, "resident": qf.QF_ENGINE_RESIDENT}[os.environ.get("AB_ENGINE", "resident")]
 import time
 ms = []
 for _ in range(3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=3, engine=eng, want_result=False)
+    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=MI, engine=eng, want_result=False)
     torch.cuda.synchronize()
     ms.append(1e3 * (time.perf_counter() - t0))
 print(min(ms[1:]))
@@ -53,7 +58,7 @@ for _ in range(reps):
         for kv in filter(None, envs.split(",")):
             k, _, v = kv.partition("=")
             env[k] = v
-        out = subprocess.run([sys.executable, "-c", code, path, cfg], capture_output=True, text=True,
+        out = subprocess.run([sys.executable, "-c", code, path, cfg, str(sweeps)], capture_output=True, text=True,
                              env=env)
         res[l].append(float(out.stdout.strip().split()[-1]))
 for l in libs:

@@ -26,7 +26,7 @@ eng = {"stream": 1, "resident": 2}.get(sys.argv[3] if len(sys.argv) > 3 else "au
 w = qfgen.workload(name)
 c = qf.Circuit.from_workload(w)
 r = qf.qf_instantiate(c, w.target_unitary(), w.initial(), max_iters=iters, engine=eng)
-out = (ctypes.c_ulonglong * 10)()
+out = (ctypes.c_ulonglong * 14)()
 qf.lib().qf_debug_polar_counts(out)
 print(f"{name} {iters} sweeps: NS calls {out[0]}, NS iterations {out[1]} "
       f"({out[1] / max(1, out[0]):.2f} per call), Jacobi sweeps {out[2]}")
@@ -36,6 +36,13 @@ if out[5]:
 if out[9]:
     print(f"  gather (all threads, before the barrier) {out[6] / out[9]:.0f}, form A {out[7] / out[9]:.0f}, "
           f"polar {out[8] / out[9]:.0f} cycles")
+
+if out[13]:
+    print(f"  WIDE overlapped phase A on warp 0: env from T {out[10] / out[13]:.0f} (incl. the u_old "
+          f"load issue), u_old staged {out[11] / out[13]:.0f}, prepare (form A + polar + L/R) "
+          f"{out[12] / out[13]:.0f} cycles ({out[13]} steps)")
+    print(f"  phase A per step: warp 0 {out[3] / out[5]:.0f}, warp 1 (sandwich) {out[4] / out[5]:.0f}; "
+          f"after the barrier (tile table + T gather) {out[6] / out[5]:.0f} cycles")
 
 rc = (ctypes.c_ulonglong * 5)()
 qf.lib().qf_debug_rows_counts(rc)
