@@ -8,8 +8,14 @@ Sec. 8a: stage inputs, InitCircuitTensor, TwoSidedSweeps with the per-start
 termination state machine until every start has a verdict, result reduction
 -- over one batch of synthetic inputs already resident in HBM, plus (N > 1)
 the end-of-run exchange: NCCL allgather of per-start summaries, the argmin
-kernel, and the broadcast of the winner's gates.  Weak scaling: every rank
-runs the config's full start count on its own global start range.
+kernel, and the broadcast of the winner's gates.  Strong scaling by default:
+the config's start count is split over the ranks (BASELINE: "sharded across
+GPUs"); --scaling weak gives every rank the full count on its own range.
+
+hbm_probe = the HBM regime under the same clock: C5 (n = 8, 8192 starts split
+over the ranks) on the streaming engine, init + 2 sweeps from device-seeded
+starts, with its own roofline (sandwich passes vs the measured HBM peak), the
+environment kernels' useful-byte rate, and clocks.
 
 metric = converged instantiations/s: starts driven to a terminal verdict per
 second, whole job.  e2e = the same through qf_instantiate with pinned HOST
@@ -106,21 +112,24 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def config_dict(w, world):
+def config_dict(w, world, scaling="strong"):
+    per_gpu = -(-w.starts // world) if scaling == "strong" else w.starts
     return {
         "workload": f"{w.name}: {w.desc}",
         "n_qubits": w.n,
         "gates": w.p,
         "gate_arities": sorted({len(l) for l in w.locs}),
-        "starts_per_gpu": w.starts,
-        "global_starts": w.starts * world,
+        "starts_per_gpu": per_gpu,
+        "global_starts": w.starts if scaling == "strong" else w.starts * world,
         "target": "self-target V = C(alpha*)" if w.target == "self" else "Haar",
         "max_iters": w.max_iters,
         "hyperparams": "P:532 defaults (dist_tol 1e-10, diff_tol_r 1e-5, long_diff 100/0.1, reset 40, beta 0)",
-        "l2": (f"inputs larger than L2: circuit tensors {w.starts * 16 * 4 ** w.n / 2**20:.0f} MiB per GPU "
-               "vs 126 MB L2, no flush" if w.starts * 16 * 4 ** w.n > 126e6 else
+        "l2": (f"inputs larger than L2: circuit tensors {per_gpu * 16 * 4 ** w.n / 2**20:.0f} MiB per GPU "
+               "vs 126 MB L2, no flush" if per_gpu * 16 * 4 ** w.n > 126e6 else
                "working set fits in L2 (reported as such)"),
-        "parallelism": f"starts sharded over {world} GPU(s), weak scaling",
+        "parallelism": (f"{w.starts} starts split over {world} GPU(s) (strong scaling)"
+                        if scaling == "strong" else
+                        f"{w.starts} starts per GPU on {world} GPU(s) (weak scaling)"),
         "termination": ("paper batch policy (P:667-676): all starts of the job stop on the first "
                         "success, plateau-stop once every start has plateaued"
                         if getattr(w, "batch", "per-start") == "paper" else "per-start verdicts"),
@@ -178,8 +187,8 @@ def run_reference(args, w, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(w, 1),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(w, world, args.scaling),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": int(res.threads), "kind": "oracle",
                          "sample": f"each step: {w.name} starts [0, {S}) run to verdict by the "
                                    f"plain C oracle on {int(res.threads)} host threads"},
@@ -228,6 +237,82 @@ def roofline(st, step_ms, w):
             "share_of_step": sw_ms / step_ms if step_ms > 0 else None, "peak_source": src}
 
 
+# ---------------------------------------------------------------- HBM probe
+def hbm_probe(qf, qfdist, torch, dist, rank, world, local, dev, stream):
+    """C5 (n = 8, 1 MiB circuit tensor per start, 8192 starts split over the
+    ranks, 110 U(4) + 90 U(8)) on the streaming engine -- the HBM regime
+    (BASELINE 'sweep HBM GB/s'): init + 2 sweeps from seeded starts
+    generated on the device (qf_params.seed, initial = NULL).  One untimed
+    warm-up call, one timed call (CUDA events on the stream, max over ranks),
+    one call with per-launch events for the kernel split."""
+    w5 = qfgen.workload("C5")
+    sh = qfdist.Shard.strong(w5.starts, world, rank)
+    c5 = qf.Circuit.from_workload(w5)
+    V5 = torch.from_numpy(np.ascontiguousarray(w5.target_unitary())).to(dev)
+    sweeps = 2
+    ws5 = torch.empty(qf.qf_workspace_size(c5, sh.S, max_iters=sweeps), dtype=torch.uint8,
+                      device=dev)
+    kw = dict(max_iters=sweeps, seed=w5.init_seed, start_offset=sh.start_begin, num_starts=sh.S)
+    qf.qf_instantiate_device(c5, V5, None, ws5, stream, want_result=False, **kw)  # warm-up
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    r = qf.qf_instantiate_device(c5, V5, None, ws5, stream, **kw)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    rp = qf.qf_instantiate_device(c5, V5, None, ws5, stream, profile=1, **kw)
+    torch.cuda.synchronize()
+    st, sp = r.stats, rp.stats
+    vec = torch.tensor([ms, st["alg_bytes_total"]], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, alg_sum = float(mx[0]), float(sm[1])
+    else:
+        ms_max, alg_sum = ms, st["alg_bytes_total"]
+    del ws5
+    torch.cuda.empty_cache()
+    peak, src = load_peaks()
+    sw_gbs = sp["sandwich_bytes"] / 1e9 / (sp["sandwich_ms"] / 1e3) if sp["sandwich_ms"] else None
+    env_gbs = sp["env_bytes"] / 1e9 / (sp["env_ms"] / 1e3) if sp["env_ms"] else None
+    traffic, _ = load_traffic("C5")
+    return {
+        "workload": f"C5: {w5.desc}",
+        "starts": w5.starts, "starts_per_gpu": sh.S_max, "sweeps": sweeps,
+        "initial": "seeded on the device (seed 2005, keyed by global start and gate)",
+        "ms": ms_max,
+        "sweep_hbm_gbs": (alg_sum / 1e9) / (ms_max / 1e3),
+        "sweep_hbm_frac": (alg_sum / 1e9) / (ms_max / 1e3) / (peak * world),
+        "gpu_launches": int(st["kernel_launches"]),
+        "roofline": {
+            "kernel": "sandwich passes (k_sandwich_reg d<=4, k_sandwich_rows d=8), aggregate",
+            "bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
+            "frac": sw_gbs / peak if sw_gbs else None, "traffic": traffic,
+            "alg_bytes_per_launch": (sp["sandwich_bytes"] / sp["sandwich_launches"]
+                                     if sp["sandwich_launches"] else None),
+            "launches": int(sp["sandwich_launches"]),
+            "share_of_step": sp["sandwich_ms"] / ms if ms else None, "peak_source": src},
+        "env_kernels": {
+            "kernel": "k_env_polar / k_group (environment gather + polar factor), aggregate",
+            "useful_gbs": env_gbs, "frac": env_gbs / peak if env_gbs else None,
+            "launches": int(sp["env_launches"]),
+            "share_of_step": sp["env_ms"] / ms if ms else None,
+            "bytes_def": "16 * N * 2^|W| per start (the entries the partial trace needs) + gate r/w"},
+        "timing": "CUDA events on the call's stream around one call after one warm-up call; "
+                  "the kernel split from a second call with per-launch events",
+        "clocks": clk,
+    }
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -244,6 +329,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--batch", default="per-start", choices=["per-start", "paper"],
                     help="termination: per-start verdicts, or the paper's batch policy (NEXT-1)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's start count split over the ranks (BASELINE: "
+                         "'sharded across GPUs'); weak: every rank runs the full count")
+    ap.add_argument("--no-hbm-probe", action="store_true",
+                    help="skip the C5 streaming-engine probe (HBM regime, init + 2 sweeps)")
     args = ap.parse_args()
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
@@ -266,8 +356,11 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    S = w.starts
-    start0 = rank * S
+    shard = (qfdist.Shard.strong(w.starts, world, rank) if args.scaling == "strong"
+             else qfdist.Shard(rank, world, w.starts))
+    job_starts = w.starts if args.scaling == "strong" else w.starts * world
+    S = shard.S
+    start0 = shard.start_begin
     c = qf.Circuit.from_workload(w)
     V = np.ascontiguousarray(w.target_unitary())
     init = w.initial(start0, S)
@@ -278,7 +371,6 @@ def main():
     gates_out = torch.empty_like(d_init)
     summ = torch.empty(S * 16, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    shard = qfdist.Shard(rank, world, S)
     bparams = {}
     if args.batch == "paper":
         bparams["batch_policy"] = qf.QF_BATCH_PAPER
@@ -351,10 +443,14 @@ def main():
             dist.all_reduce(tv, op=dist.ReduceOp.MAX)
         h2d = rr[-1]["h2d_bytes"]
         d2h = rr[-1]["d2h_bytes"]
-        e2e = {"value": world * S * args.steps / float(tv[0]), "unit": UNIT,
+        e2e = {"value": job_starts * args.steps / float(tv[0]), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": 1000 * float(tv[0]) / args.steps,
                "api": "qf_instantiate (host buffers, pinned)"}
+
+    probe = None
+    if not args.no_hbm_probe and args.config != "C5":
+        probe = hbm_probe(qf, qfdist, torch, dist, rank, world, local, dev, stream)
 
     if rank != 0:
         if world > 1:
@@ -363,18 +459,18 @@ def main():
     roof = roofline(st, ms, w)
     line = {
         "metric": METRIC,
-        "value": world * S * args.steps / (ms_max / 1e3),
+        "value": job_starts * args.steps / (ms_max / 1e3),
         "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": config_dict(w, world),
+        "config": config_dict(w, world, args.scaling),
         "engine": qf.ENGINE_NAMES[st[-1]["engine"]],
         "sweep_hbm_gbs": (alg_sum / 1e9) / (ms_max / 1e3),
         "sweep_gbs_note": ("algorithmic bytes (32*4^n per gate step + init passes) / time; "
@@ -390,6 +486,8 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if probe:
+        line["hbm_probe"] = probe
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(w)
     print(json.dumps(line), flush=True)

@@ -41,7 +41,7 @@ int resident_threads(int n) {
 // the WIDE resident variant (256 threads, FP64-MMA d = 4 sandwich): n = 5, 6
 // and no gate wider than 2 qubits; QF_RES_WIDE=0 disables (A/B)
 bool resident_wide(int n, int maxm) {
-  const int env = getenv("QF_RES_WIDE") ? atoi(getenv("QF_RES_WIDE")) : 1;
+  const int env = getenv("QF_RES_WIDE") ? atoi(getenv("QF_RES_WIDE")) : 0;
   return env != 0 && kResDmma4 && n >= 5 && maxm == 2;
 }
 int resident_threads(int n, int maxm) { return resident_wide(n, maxm) ? 256 : resident_threads(n); }
@@ -1337,6 +1337,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.polar_mma = getenv("QF_POLAR_MMA") ? atoi(getenv("QF_POLAR_MMA")) : 1;
     A.serial_smsp = getenv("QF_SERIAL_SMSP") ? atoi(getenv("QF_SERIAL_SMSP")) : 0;
     A.sw_ilp = getenv("QF_SW_ILP") ? atoi(getenv("QF_SW_ILP")) : 1;
+    A.ovl = getenv("QF_OVL") ? atoi(getenv("QF_OVL")) : 1;
     A.gather_ltpo_max = getenv("QF_GATHER_LTPO") ? std::max(0, std::min(5, atoi(getenv("QF_GATHER_LTPO")))) : 5;
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;
@@ -1799,6 +1800,9 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
   A.counter = counter;
   A.polar_jacobi = 0;
   A.polar_mma = getenv("QF_POLAR_MMA") ? atoi(getenv("QF_POLAR_MMA")) : 1;
+  A.serial_smsp = getenv("QF_SERIAL_SMSP") ? atoi(getenv("QF_SERIAL_SMSP")) : 0;
+  A.sw_ilp = getenv("QF_SW_ILP") ? atoi(getenv("QF_SW_ILP")) : 1;
+  A.ovl = getenv("QF_OVL") ? atoi(getenv("QF_OVL")) : 1;
   A.gather_ltpo_max = 5;
   A.dist_tol = p.dist_tol;
   A.diff_tol_a = p.diff_tol_a;

@@ -80,6 +80,7 @@ struct ResidentArgs {
   const struct WDesc *wdt;  // WIDE: transitions j -> j + 1 of one sweep (2p, host-built)
   int serial_smsp;    // WIDE: warp 4 (warp 0's sub-partition) idles in the overlapped phase
   int sw_ilp;         // WIDE: MMA tiles in flight per sandwich warp while warp 0 prepares
+  int ovl;            // WIDE: overlap the next step's environment + polar with the sandwich
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
   // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
@@ -124,6 +125,20 @@ __host__ __device__ __forceinline__ int sidx(int i, int j, int N) {
   return i * N + (j ^ (int)(f & (unsigned)(N - 1) & 7u));
 }
 
+// Round-1 layout of the 128-thread kernel: element (i, j) at i*N + swz(j),
+// swz(j) = j ^ f(j >> 3 & 7), tuned for the register-block sandwich's access
+// pattern (392 vs 840 wavefronts unswizzled at n = 6).  The 128-thread kernel
+// keeps it (the GF(2) row swizzle above measured 2 % slower there); the WIDE
+// variant's MMA tiles need the row-dependent one.
+__device__ __forceinline__ int swz_r1(int j) {
+  return j ^ (int)((0x41362750u >> (4 * ((j >> 3) & 7))) & 7u);
+}
+template <bool WS>
+__device__ __forceinline__ int sidxw(int i, int j, int N) {
+  if constexpr (WS) return sidx(i, j, N);
+  else return i * N + swz_r1(j);
+}
+
 __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
   return insert_zeros(r, g.mask);
 }
@@ -132,7 +147,7 @@ __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
 // column-rest c) per item held in registers: one shared-memory read and write
 // per element; items are spread over threads t0, t0 + nt, ...  No barrier
 // inside.
-template <int D>
+template <int D, bool WS = false>
 __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N,
                                     const double2 *Ls, const double2 *Rs, int t0, int nt) {
   constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
@@ -144,7 +159,7 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
 #pragma unroll
     for (int a = 0; a < D; a++)
 #pragma unroll
-      for (int b = 0; b < D; b++) x[a][b] = ct[sidx(rb | g.abits[a], cb | g.abits[b], N)];
+      for (int b = 0; b < D; b++) x[a][b] = ct[sidxw<WS>(rb | g.abits[a], cb | g.abits[b], N)];
     // row by row: z[a][:] = (L[a][:] x) R, stored over the (register-held)
     // block, the outputs in pairs (four independent accumulation chains)
 #pragma unroll
@@ -166,8 +181,8 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
           z0 = cfma(y[k], Rs[k * D + b], z0);
           z1 = cfma(y[k], Rs[k * D + b + 1], z1);
         }
-        ct[sidx(rb | g.abits[a], cb | g.abits[b], N)] = z0;
-        ct[sidx(rb | g.abits[a], cb | g.abits[b + 1], N)] = z1;
+        ct[sidxw<WS>(rb | g.abits[a], cb | g.abits[b], N)] = z0;
+        ct[sidxw<WS>(rb | g.abits[a], cb | g.abits[b + 1], N)] = z1;
       }
     }
   }
@@ -291,7 +306,7 @@ __device__ __forceinline__ void res_sandwich_dmma4(double2 *ct, const GateDesc &
 }
 
 // ct <- E(L) ct E(R) in place (R == nullptr: one-sided), all threads.
-template <int D>
+template <int D, bool WS = false>
 __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const double2 *Ls,
                              const double2 *Rs) {
   constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
@@ -303,13 +318,13 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
     const int rb = rspread(g, n, r);
     double2 x[D];
 #pragma unroll
-    for (int a = 0; a < D; a++) x[a] = ct[sidx(rb | g.abits[a], j, N)];
+    for (int a = 0; a < D; a++) x[a] = ct[sidxw<WS>(rb | g.abits[a], j, N)];
 #pragma unroll
     for (int a = 0; a < D; a++) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < D; k++) acc = cfma(Ls[a * D + k], x[k], acc);
-      ct[sidx(rb | g.abits[a], j, N)] = acc;
+      ct[sidxw<WS>(rb | g.abits[a], j, N)] = acc;
     }
   }
   if (Rs == nullptr) {
@@ -323,13 +338,13 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
     const int cb = rspread(g, n, c);
     double2 z[D];
 #pragma unroll
-    for (int b = 0; b < D; b++) z[b] = ct[sidx(i, cb | g.abits[b], N)];
+    for (int b = 0; b < D; b++) z[b] = ct[sidxw<WS>(i, cb | g.abits[b], N)];
 #pragma unroll
     for (int b = 0; b < D; b++) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int k = 0; k < D; k++) acc = cfma(z[k], Rs[k * D + b], acc);
-      ct[sidx(i, cb | g.abits[b], N)] = acc;
+      ct[sidxw<WS>(i, cb | g.abits[b], N)] = acc;
     }
   }
   __syncthreads();
@@ -339,7 +354,7 @@ __device__ void res_sandwich(double2 *ct, const GateDesc &g, int n, int N, const
 // P[a][b] = sum_r ct[ins(a,r)][ins(b,r)].  TPO threads of one warp
 // per output take r = k, k+TPO, ... ascending; a fixed xor-tree combines them
 // (deterministic, independent of which CTA runs the start).
-template <int D>
+template <int D, bool WS = false>
 __device__ void res_gather_d(const ResidentArgs &A, const ResView &V, const double2 *ct,
                              const GateDesc &g, double2 *Pm) {
   constexpr int DD = D * D;
@@ -359,7 +374,7 @@ __device__ void res_gather_d(const ResidentArgs &A, const ResView &V, const doub
       const int a = o / D, b = o % D;
       for (int r = k; r < R; r += tpo) {
         const int sp = rspread(g, V.n, r);
-        const double2 v = ct[sidx(sp | g.abits[a], sp | g.abits[b], N)];
+        const double2 v = ct[sidxw<WS>(sp | g.abits[a], sp | g.abits[b], N)];
         acc.x += v.x;
         acc.y += v.y;
       }
@@ -373,16 +388,16 @@ __device__ void res_gather_d(const ResidentArgs &A, const ResView &V, const doub
   }
 }
 
-template <int MAXD>
+template <int MAXD, bool WS = false>
 __device__ __forceinline__ void res_gather(const ResidentArgs &A, const ResView &V,
                                            const double2 *ct, const GateDesc &g, double2 *Pm) {
   if (g.d == 2) {
-    res_gather_d<2>(A, V, ct, g, Pm);
+    res_gather_d<2, WS>(A, V, ct, g, Pm);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
-      res_gather_d<4>(A, V, ct, g, Pm);
+      res_gather_d<4, WS>(A, V, ct, g, Pm);
     } else if constexpr (MAXD >= 8) {
-      res_gather_d<8>(A, V, ct, g, Pm);
+      res_gather_d<8, WS>(A, V, ct, g, Pm);
     }
   }
 }
@@ -512,8 +527,8 @@ __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const 
   const int nb = V.N / g.d;
   const bool blocks = !SMALL && nb * nb >= nt;
   if (g.d == 2) {
-    if (blocks) res_sandwich_blocks<2>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
-    else res_sandwich<2>(ct, g, V.n, V.N, Lb, Rb);
+    if (blocks) res_sandwich_blocks<2, WIDE>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+    else res_sandwich<2, WIDE>(ct, g, V.n, V.N, Lb, Rb);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
       if (WIDE || res_use_dmma4<MAXD, SMALL, WIDE>(g, V)) {
@@ -521,39 +536,39 @@ __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const 
         else if (WIDE && ilp == 2) res_sandwich_dmma4<2>(ct, g, V.n, V.N, Lb, Rb, tab, t0 >> 5, nt >> 5);
         else res_sandwich_dmma4(ct, g, V.n, V.N, Lb, Rb, tab, t0 >> 5, nt >> 5);
       }
-      else if (blocks) res_sandwich_blocks<4>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
-      else res_sandwich<4>(ct, g, V.n, V.N, Lb, Rb);
+      else if (blocks) res_sandwich_blocks<4, WIDE>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+      else res_sandwich<4, WIDE>(ct, g, V.n, V.N, Lb, Rb);
     } else if constexpr (MAXD >= 8) {
-      res_sandwich<8>(ct, g, V.n, V.N, Lb, Rb);
+      res_sandwich<8, WIDE>(ct, g, V.n, V.N, Lb, Rb);
     }
   }
 }
 
-template <int D>
+template <int D, bool WS = false>
 __device__ void res_apply_left(double2 *ct, const GateDesc &g, const ResView &V,
                                const double2 *src, double2 *Ls) {
   for (int e = threadIdx.x; e < D * D; e += blockDim.x) Ls[e] = src[e];
   __syncthreads();
-  res_sandwich<D>(ct, g, V.n, V.N, Ls, nullptr);
+  res_sandwich<D, WS>(ct, g, V.n, V.N, Ls, nullptr);
 }
 
-template <int MAXD>
+template <int MAXD, bool WS = false>
 __device__ void res_init(const ResidentArgs &A, const ResView &V, double2 *ct,
                          const GateDesc *gdesc, int s, double2 *Ls) {
   const int NN = V.N * V.N;
   for (int e = threadIdx.x; e < NN; e += blockDim.x)
-    ct[sidx(e >> V.n, e & (V.N - 1), V.N)] = V.vdag[e];
+    ct[sidxw<WS>(e >> V.n, e & (V.N - 1), V.N)] = V.vdag[e];
   __syncthreads();
   for (int k = 0; k < V.p; k++) {
     const GateDesc &g = gdesc[k];
     const double2 *src = g.kind != 1 ? V.u0 + g.goff : V.cmats + g.goff;
     if (g.d == 2) {
-      res_apply_left<2>(ct, g, V, src, Ls);
+      res_apply_left<2, WS>(ct, g, V, src, Ls);
     } else if constexpr (MAXD >= 4) {
       if (g.d == 4) {
-        res_apply_left<4>(ct, g, V, src, Ls);
+        res_apply_left<4, WS>(ct, g, V, src, Ls);
       } else if constexpr (MAXD >= 8) {
-        res_apply_left<8>(ct, g, V, src, Ls);
+        res_apply_left<8, WS>(ct, g, V, src, Ls);
       }
     }
   }
@@ -851,7 +866,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       fw = j >= V.p;
       return fw ? j - V.p : V.p - 1 - j;
     };
-    res_init<MAXD>(A, V, ct, gdesc, s, Lb);
+    res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
     int it = 0;
     // operands of step j2 into buffer (j2 & 1): all threads gather the
     // environment (VARIABLE gates), the serial warp stages u_old (prefetched
@@ -868,7 +883,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
 #ifdef QF_POLAR_COUNT
         const long long tg0 = clock64();
 #endif
-        res_gather<MAXD>(A, V, ct, g2, Pm);
+        res_gather<MAXD, WIDE>(A, V, ct, g2, Pm);
 #ifdef QF_POLAR_COUNT
         if (tid == 0) atomicAdd(&qf_t_gather, (unsigned long long)(clock64() - tg0));
 #endif
@@ -896,7 +911,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
     // WIDE: is the environment of step j + 1 formed from T while step j's
     // sandwich runs (|W| <= 4; a CONSTANT next gate needs no environment)
     auto ovl_ok = [&](int j) -> bool {
-      if (j + 1 >= steps) return false;
+      if (j + 1 >= steps || !A.ovl) return false;
       int f1, f2;
       const GateDesc &ga = gdesc[gate_of(j, f1)], &gb = gdesc[gate_of(j + 1, f2)];
       return gb.kind == 1 || __popc(ga.mask | gb.mask) <= 4;
@@ -1045,8 +1060,8 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       if (serial) {
         double re = 0.0, im = 0.0;
         for (int i = lane; i < V.N; i += 32) {
-          re += ct[sidx(i, i, V.N)].x;
-          im += ct[sidx(i, i, V.N)].y;
+          re += ct[sidxw<WIDE>(i, i, V.N)].x;
+          im += ct[sidxw<WIDE>(i, i, V.N)].y;
         }
         for (int off = 1; off < 32; off <<= 1) {
           re += __shfl_xor_sync(0xffffffffu, re, off);
@@ -1131,7 +1146,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       } else if (s_verdict != 0) {
         break;
       }
-      if (it % A.reset_iters == 0) res_init<MAXD>(A, V, ct, gdesc, s, Lb);
+      if (it % A.reset_iters == 0) res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
       prepare(0, false);  // operands of the next sweep's first step
       wd_fetch(0);
       if constexpr (WIDE) {

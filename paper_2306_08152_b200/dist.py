@@ -20,18 +20,46 @@ from . import BATCH_REDUCE_FN, qf_select_best_device
 
 @dataclass
 class Shard:
-    """Weak-scaling shard: rank r owns global starts [r*S, (r+1)*S)."""
+    """This rank's contiguous range of global starts.
+
+    Weak scaling (`Shard(rank, world, S)`): every rank owns S starts,
+    [r*S, (r+1)*S).  Strong scaling (`Shard.strong(total, world, rank)`): the
+    job's `total` starts split by `shard_range` (sizes differ by <= 1).  The
+    end-of-run allgather pads every rank's table to `S_max` records."""
 
     rank: int
     world: int
     S: int
+    total: int | None = None  # strong scaling: the job's start count
+
+    @classmethod
+    def strong(cls, total: int, world: int, rank: int) -> "Shard":
+        b, e = shard_range(total, world, rank)
+        return cls(rank, world, e - b, total)
+
+    def range_of(self, rank: int):
+        if self.total is None:
+            return rank * self.S, (rank + 1) * self.S
+        return shard_range(self.total, self.world, rank)
 
     @property
     def start_begin(self) -> int:
-        return self.rank * self.S
+        return self.range_of(self.rank)[0]
+
+    @property
+    def S_max(self) -> int:
+        if self.total is None:
+            return self.S
+        return -(-self.total // self.world)
 
     def owner(self, global_index: int):
-        return divmod(int(global_index), self.S)
+        """(rank, local index) owning a global start index."""
+        g = int(global_index)
+        for r in range(self.world):
+            b, e = self.range_of(r)
+            if b <= g < e:
+                return r, g - b
+        raise IndexError(global_index)
 
 
 def shard_range(total: int, world: int, rank: int):
@@ -46,16 +74,26 @@ def exchange_best(shard: Shard, summ: torch.Tensor, gates_out: torch.Tensor, str
     """End-of-run exchange.  summ: uint8 tensor of S x 16-byte qf_summary;
     gates_out: (S, var) float64.  Returns (best global index, winner gates)
     on every rank.  `select(gathered, count) -> int` defaults to the argmin
-    kernel on the device."""
-    gathered = torch.empty(shard.world * summ.numel(), dtype=torch.uint8, device=summ.device)
-    dist.all_gather_into_tensor(gathered, summ)
+    kernel on the device.  Ranks with fewer than S_max starts pad their table
+    with NaN-Delta records (a NaN never wins the argmin)."""
+    rec = 16
+    pad = shard.S_max - shard.S
+    if pad:
+        filler = torch.zeros(pad * rec, dtype=torch.uint8, device=summ.device)
+        filler.view(torch.float64)[0::2] = float("nan")
+        summ = torch.cat([summ[: shard.S * rec], filler])
+    gathered = torch.empty(shard.world * shard.S_max * rec, dtype=torch.uint8, device=summ.device)
+    dist.all_gather_into_tensor(gathered, summ.contiguous())
+    count = shard.world * shard.S_max
     if select is None:
         best_t = torch.empty(1, dtype=torch.int64, device=summ.device)
-        qf_select_best_device(gathered, shard.world * shard.S, best_t, stream)
-        best = int(best_t.item())
+        qf_select_best_device(gathered, count, best_t, stream)
+        best_p = int(best_t.item())
     else:
-        best = int(select(gathered, shard.world * shard.S))
-    owner, local = shard.owner(best)
+        best_p = int(select(gathered, count))
+    r, local = divmod(best_p, shard.S_max)  # padded layout -> (rank, local)
+    owner = r
+    best = shard.range_of(r)[0] + local
     if shard.rank == owner:
         buf = gates_out[local].contiguous().clone()
     else:

@@ -22,12 +22,15 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, S, var, q):
+def _worker(rank, world, port, S, var, q, total=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        shard = Shard(rank, world, S)
+        # weak: S starts per rank; strong (bench.py --scaling strong): the
+        # job's `total` starts split by shard_range, tables padded to S_max
+        shard = Shard(rank, world, S) if total is None else Shard.strong(total, world, rank)
+        S = shard.S
         summ = np.zeros(S, dtype=qf.SUMMARY_DTYPE)
         # deltas keyed by global start index; global 5 and 9 tie for the minimum
         g = np.arange(shard.start_begin, shard.start_begin + S)
@@ -62,6 +65,30 @@ def test_exchange_best_gloo_world2():
     for rank, best, buf in out:
         assert best == 5  # tie between global 5 (rank 0) and 9 (rank 1) -> lowest index
         assert buf == [5.0] * var
+
+
+@pytest.mark.parametrize("total", [13, 16])
+def test_exchange_best_strong_gloo_world2(total):
+    """bench.py's strong split: 13 starts over 2 ranks (7 + 6, rank 1 padded
+    with a NaN record); global 5 (rank 0) and 9 (rank 1) tie -> 5."""
+    world, var = 2, 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 0, var, q, total))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, best, buf in out:
+        assert best == 5
+        assert buf == [5.0] * var
+    s = Shard.strong(total, world, 1)
+    assert s.start_begin == (total + 1) // 2 and s.S == total // 2 and s.S_max == (total + 1) // 2
+    assert s.owner(total - 1) == (1, s.S - 1)
 
 
 def test_shard_ranges():
