@@ -20,7 +20,11 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "qf_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# ORACLE_SANITIZE=1: an AddressSanitizer + UndefinedBehaviorSanitizer build
+# (liboracle_asan.so; run under LD_PRELOAD=$(gcc -print-file-name=libasan.so),
+# ASAN_OPTIONS=detect_leaks=0) -- tools/oracle_sanitize.sh
+_SAN = os.environ.get("ORACLE_SANITIZE") == "1"
+_LIB = os.path.join(_HERE, "liboracle_asan.so" if _SAN else "liboracle.so")
 
 VARIABLE, CONSTANT, RZ = 0, 1, 2
 RUNNING, CONVERGED, PLATEAU_SHORT, PLATEAU_LONG, MAX_ITER, NUMERIC_FAIL, BATCH_STOPPED = range(7)
@@ -32,9 +36,11 @@ def build(force: bool = False) -> str:
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "qf_oracle.h"))
     ):
         tmp = _LIB + f".tmp{os.getpid()}"
+        san = (["-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined",
+                "-fno-sanitize-recover=undefined"] if _SAN else [])
         subprocess.check_call(
             ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-             "-D_GNU_SOURCE", "-fPIC", "-shared", "-pthread", _SRC, "-o", tmp, "-lm"]
+             "-D_GNU_SOURCE", "-fPIC", "-shared", "-pthread", *san, _SRC, "-o", tmp, "-lm"]
         )
         os.replace(tmp, _LIB)
     return _LIB

@@ -113,6 +113,10 @@ _lib = None
 def lib():
     """Load (building in-tree first if stale) libqfactor.so."""
     global _lib
+    if _lib is None and os.environ.get("QF_LIB"):  # an alternative build (checked / A-B)
+        L = ctypes.CDLL(os.environ["QF_LIB"])
+        _declare(L)
+        _lib = L
     if _lib is None:
         if _build.needs_build():
             if not os.path.exists(_build.NVCC):

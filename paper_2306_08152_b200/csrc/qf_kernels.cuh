@@ -24,6 +24,25 @@
 namespace qf {
 
 constexpr int kMaxQubits = 12;
+
+// Device bounds checks (compute-sanitizer is closed on the GPU pool): a
+// -DQF_DEVICE_CHECKS build (tools/checked_build.py) traps with the failing
+// index on any circuit-tensor / gate / tile index out of range; the product
+// build compiles them out.
+#ifdef QF_DEVICE_CHECKS
+#define QF_DCHECK(cond, what, a, b)                                                        \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("QF_DCHECK failed: %s (%lld, %lld) block %d thread %d\n", what, (long long)(a), \
+             (long long)(b), (int)blockIdx.x, (int)threadIdx.x);                          \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define QF_DCHECK(cond, what, a, b) \
+  do {                              \
+  } while (0)
+#endif
 #ifdef QF_POLAR_COUNT
 __device__ unsigned long long qf_polar_sweeps;  // microbenchmark instrumentation only
 __device__ unsigned long long qf_ns_iters, qf_ns_calls;
@@ -852,6 +871,7 @@ __device__ __forceinline__ void warp_gather_pt(const Bits &B, const double2 *cts
     const int sp = spread_rest(B, r);
 #pragma unroll
     for (int q = 0; q < OPL; q++) {
+      QF_DCHECK((sp | ia[q]) < N && (sp | ib[q]) < N, "gather index", sp | ia[q], sp | ib[q]);
       const double2 v = cts[(long long)(sp | ia[q]) * N + (sp | ib[q])];
       acc[q].x += v.x;
       acc[q].y += v.y;
@@ -1619,7 +1639,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sandwich_reg(const SandwichArgs A)
 #pragma unroll
     for (int a = 0; a < D; a++)
 #pragma unroll
-      for (int b = 0; b < D; b++) x[a][b] = cts[base + A.b.abits[a] * N + A.b.abits[b]];
+      for (int b = 0; b < D; b++) {
+        QF_DCHECK(base + A.b.abits[a] * N + A.b.abits[b] < (long long)N * N, "reg sandwich index",
+                  base, A.b.abits[a] * N + A.b.abits[b]);
+        x[a][b] = cts[base + A.b.abits[a] * N + A.b.abits[b]];
+      }
     // left: column by column, in place in registers
 #pragma unroll
     for (int b = 0; b < D; b++) {

@@ -122,7 +122,11 @@ constexpr unsigned kSwColT = 0x72143650u;   // column bits 3..5 -> XOR of {5, 6,
 __host__ __device__ __forceinline__ int sidx(int i, int j, int N) {
   const unsigned f = (kSwRowLo >> (4 * (i & 7))) ^ (kSwRowHi >> (4 * ((i >> 3) & 7))) ^
                      (kSwColT >> (4 * ((j >> 3) & 7)));
-  return i * N + (j ^ (int)(f & (unsigned)(N - 1) & 7u));
+  const int idx = i * N + (j ^ (int)(f & (unsigned)(N - 1) & 7u));
+#ifdef __CUDA_ARCH__
+  QF_DCHECK(i >= 0 && i < N && j >= 0 && j < N, "tensor (row, col)", i, j);
+#endif
+  return idx;
 }
 
 // Round-1 layout of the 128-thread kernel: element (i, j) at i*N + swz(j),
@@ -136,7 +140,10 @@ __device__ __forceinline__ int swz_r1(int j) {
 template <bool WS>
 __device__ __forceinline__ int sidxw(int i, int j, int N) {
   if constexpr (WS) return sidx(i, j, N);
-  else return i * N + swz_r1(j);
+  else {
+    QF_DCHECK(i >= 0 && i < N && j >= 0 && j < N, "tensor (row, col)", i, j);
+    return i * N + swz_r1(j);
+  }
 }
 
 __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
@@ -259,6 +266,8 @@ __device__ __forceinline__ void res_sandwich_dmma4(double2 *ct, const GateDesc &
     for (int u = 0; u < ILP; u++) {
       const int t = t0 + u * nw;
       at[u] = tab[t < ntile ? t : t0];  // idle slots redo tile t0 (not stored)
+      QF_DCHECK((at[u] ^ ld_lane) >= 0 && (at[u] ^ ld_lane) < N * N && (at[u] ^ st_lane) < N * N,
+                "MMA tile address", at[u] ^ ld_lane, at[u] ^ st_lane);
       x[u] = ct[at[u] ^ ld_lane];
     }
     // issue order matters (in-order issue, 26-cycle MMA latency): the first
@@ -470,6 +479,7 @@ __device__ void res_prepare_d(const ResidentArgs &A, const ResView &V, const dou
                               double2 *Uo, double2 *Pm, double2 *Am, double2 *Vm, int lane) {
   constexpr int DD = D * D;
   if (g.kind != 1) {  // VARIABLE or RZ
+    QF_DCHECK(g.goff >= 0 && g.goff + DD <= A.gstride + (A.probs ? 1 << 30 : 0), "gate offset", g.goff, DD);
     double2 *u = V.u0 + g.goff;
     double2 *vs = (A.vstore && D > 2)
                       ? A.vstore + (long long)s * A.vstride + g.voff + (forward ? DD : 0)
