@@ -118,7 +118,7 @@ typedef struct {
   int32_t long_diff_count;/* >= 0; 0 disables the long-plateau test         */
   double long_diff_r;     /* >= 0                                           */
   int32_t min_iters;      /* >= 0                                           */
-  int32_t max_iters;      /* >= 0; 0 returns the initial Delta, MAX_ITER    */
+  int32_t max_iters;      /* 0..1e7; 0 returns the initial Delta, MAX_ITER  */
   int32_t reset_iters;    /* >= 1; rebuild the circuit tensor every k sweeps*/
   double beta;            /* in [0, 1]; SVD of (1-beta)E + beta u^dagger    */
   int32_t num_starts;     /* S >= 1 (starts of this call / shard)           */

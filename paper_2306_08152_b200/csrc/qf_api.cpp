@@ -127,11 +127,16 @@ double unitarity_error(const double *M, int d) {
   return worst;
 }
 
+constexpr int kMaxItersLimit = 10000000;
+
 qf_status check_params(const qf_circuit_s *c, const qf_params *p) {
   if (!c) return fail(QF_E_ARG, "circuit is NULL");
   if (!p) return fail(QF_E_ARG, "params is NULL");
   if (p->num_starts < 1) return fail(QF_E_ARG, "num_starts must be >= 1");
   if (p->max_iters < 0) return fail(QF_E_ARG, "max_iters must be >= 0");
+  // per-sweep host bookkeeping and pinned words scale with max_iters
+  // (~40 bytes per sweep): 1e7 sweeps (100x the paper's 1e5) at most
+  if (p->max_iters > kMaxItersLimit) return fail(QF_E_ARG, "max_iters must be <= 10000000");
   if (p->min_iters < 0) return fail(QF_E_ARG, "min_iters must be >= 0");
   if (p->reset_iters < 1) return fail(QF_E_ARG, "reset_iters must be >= 1");
   if (p->long_diff_count < 0) return fail(QF_E_ARG, "long_diff_count must be >= 0");

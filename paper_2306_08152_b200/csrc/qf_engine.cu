@@ -214,6 +214,9 @@ __global__ void k_seeded_starts(double *G, long long S, long long start_offset,
   }
 }
 
+// fault injection for tests (QF_DEBUG_POISON): one start's tensor non-finite
+__global__ void k_poison(double2 *ct) { ct[0] = make_double2(NAN, NAN); }
+
 // unitarity of every VARIABLE initial gate: one thread per (start, gate)
 __global__ void k_check_gates(const double *G, long long S, int nvar, const int2 *tab,
                               int var_doubles, double tol, int *bad) {
@@ -375,13 +378,21 @@ Layout make_layout(const qf_circuit_s &c, const qf_params &p) {
       L.vstride += 2LL << (2 * c.arity[k]);
       L.nvslots += 2;
     }
+#ifdef QF_WARM_STARTS
   L.vstore = take(std::max<size_t>(1, S * (size_t)L.vstride) * 16);
+#else
+  L.vstore = take(16);  // warm starts are an experiment build (QF_WARM_STARTS) only
+#endif
   L.vslots = take((size_t)std::max(1, L.nvslots) * 8);
   L.gdesc = take((size_t)std::max(1, c.p) * sizeof(GateDesc));
   L.wdesc = take((size_t)std::max(1, 2 * c.p) * sizeof(WDesc));  // WIDE resident transitions
   L.plat = take(S * 4);
   L.gops = take(S * 128 * 16);  // grouped steps: Lp, Rp (<= 8 x 8) per start
-  L.bcnt = take((3 * ((size_t)std::max(0, p.max_iters) + 1) + 2) * 4);  // resident batch counts
+  // resident batch policy: per-sweep counts (3 words per sweep) + the grid
+  // barrier words; only a call that can take that path gets them
+  const bool res_batch = p.batch_policy == QF_BATCH_PAPER && p.batch_reduce == nullptr &&
+                         c.n <= kResidentMaxQubits;
+  L.bcnt = take(res_batch ? (3 * ((size_t)std::max(0, p.max_iters) + 1) + 2) * 4 : 16);
   L.total = o;
   return L;
 }
@@ -543,7 +554,9 @@ struct Engine {
       const std::string v(e);
       sw_kind = v == "rows" ? 1 : v == "tile" ? 2 : v == "reg" ? 3 : v == "regtile" ? 4 : 0;
     }
+#ifdef QF_WARM_STARTS  // experiment build only: the workspace then holds the warm-start store
     if (const char *e = getenv("QF_WARM")) warm = std::string(e) == "1";
+#endif
     if (const char *e = getenv("QF_POLAR")) polar_jacobi = std::string(e) == "jacobi";
     voff.assign(c.p, -1);
     long long o = 0;
@@ -1338,6 +1351,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.serial_smsp = getenv("QF_SERIAL_SMSP") ? atoi(getenv("QF_SERIAL_SMSP")) : 0;
     A.sw_ilp = getenv("QF_SW_ILP") ? atoi(getenv("QF_SW_ILP")) : 1;
     A.ovl = getenv("QF_OVL") ? atoi(getenv("QF_OVL")) : 1;
+    A.poison = getenv("QF_DEBUG_POISON") ? atoi(getenv("QF_DEBUG_POISON")) : -1;
     A.gather_ltpo_max = getenv("QF_GATHER_LTPO") ? std::max(0, std::min(5, atoi(getenv("QF_GATHER_LTPO")))) : 5;
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;
@@ -1396,6 +1410,14 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   int wave = S;
   if (!batch && p.max_iters > 0) wave = wave_size(S, (long long)N * N * 16);
   if (wave >= S || batch || p.max_iters == 0) QF_CHECK(E.init_ct());
+  if (const char *e = getenv("QF_DEBUG_POISON")) {  // fault injection (NUMERIC_FAIL tests)
+    const int ps = atoi(e);
+    if (ps >= 0 && ps < S && (wave >= S || batch)) {
+      k_poison<<<1, 1, 0, st>>>(E.ct() + (size_t)ps * N * N);
+      E.launches++;
+      QF_CHECK(cudaGetLastError());
+    }
+  }
 
   // ---- a3..a7: sweeps until every start has a verdict
   // ---- one sweep's launches (a3..a7); replayed from a CUDA graph after the
@@ -1803,6 +1825,7 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
   A.serial_smsp = getenv("QF_SERIAL_SMSP") ? atoi(getenv("QF_SERIAL_SMSP")) : 0;
   A.sw_ilp = getenv("QF_SW_ILP") ? atoi(getenv("QF_SW_ILP")) : 1;
   A.ovl = getenv("QF_OVL") ? atoi(getenv("QF_OVL")) : 1;
+  A.poison = -1;
   A.gather_ltpo_max = 5;
   A.dist_tol = p.dist_tol;
   A.diff_tol_a = p.diff_tol_a;

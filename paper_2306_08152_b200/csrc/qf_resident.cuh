@@ -81,6 +81,7 @@ struct ResidentArgs {
   int serial_smsp;    // WIDE: warp 4 (warp 0's sub-partition) idles in the overlapped phase
   int sw_ilp;         // WIDE: MMA tiles in flight per sandwich warp while warp 0 prepares
   int ovl;            // WIDE: overlap the next step's environment + polar with the sandwich
+  int poison;         // >= 0: this start's tensor is set non-finite after init (tests only)
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
   // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
@@ -877,6 +878,10 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       return fw ? j - V.p : V.p - 1 - j;
     };
     res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
+    if (A.poison >= 0) {  // fault injection for the NUMERIC_FAIL tests (QF_DEBUG_POISON)
+      if (s == A.poison && tid == 0) ct[0] = make_double2(NAN, NAN);
+      __syncthreads();
+    }
     int it = 0;
     // operands of step j2 into buffer (j2 & 1): all threads gather the
     // environment (VARIABLE gates), the serial warp stages u_old (prefetched
@@ -950,7 +955,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       }
     }
     for (;;) {
-      if (WIDE && A.max_iters > 0) {
+      if (WIDE && A.max_iters > 0 && !s_fail) {
         for (int j = 0; j < steps; j++) {
           int fw;
           const GateDesc &g = gdesc[gate_of(j, fw)];
@@ -1026,7 +1031,9 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
 #endif
         }
         it++;
-      } else if (A.max_iters > 0) {
+      } else if (A.max_iters > 0 && s_fail) {
+        it++;  // a failed start (batch policy) skips its sweep
+      } else if (A.max_iters > 0 && !s_fail) {
         for (int j = 0; j < steps; j++) {
           int fw;
           const GateDesc &g = gdesc[gate_of(j, fw)];
@@ -1103,10 +1110,13 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
               if (v == 0 && it >= A.max_iters) v = 4;
             }
           }
+          const bool failed_before = A.batch && s_fail;
           if (A.batch && it > 0) {
             // the batch decides (reading R22): plateaus do not
-            // stop a start; a failed start stops counting (it keeps sweeping
-            // NaNs until the batch ends, its verdict fixed)
+            // stop a start; a failed start stops: it skips its sweeps while
+            // the batch runs on (only joining the grid barriers) and keeps
+            // the Delta / sweep count of the sweep where it failed, as the
+            // streaming engine's compaction drops it
             if (v == 5 || s_fail) {
               s_fail = 1;
               v = 5;
@@ -1121,8 +1131,10 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
           } else {
             s_verdict = v;
           }
-          A.delta[s] = c;
-          A.iters[s] = it;
+          if (!failed_before) {
+            A.delta[s] = c;
+            A.iters[s] = it;
+          }
           if (!(A.batch && it > 0)) A.verdict[s] = v;
         }
         if (A.R > 0 && it >= 1 && it <= A.R) {
@@ -1156,6 +1168,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       } else if (s_verdict != 0) {
         break;
       }
+      if (s_fail) continue;  // a failed start (batch policy): nothing to prepare
       if (it % A.reset_iters == 0) res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
       prepare(0, false);  // operands of the next sweep's first step
       wd_fetch(0);

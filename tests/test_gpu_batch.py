@@ -150,3 +150,31 @@ def test_batch_resident_matches_streaming():
     assert a.stats["engine"] == qf.QF_ENGINE_RESIDENT and b.stats["engine"] == qf.QF_ENGINE_STREAM
     assert np.array_equal(a.verdict, b.verdict) and np.array_equal(a.iters, b.iters)
     assert np.abs(a.delta - b.delta).max() < TOL
+
+
+@pytest.mark.parametrize("policy", [qf.QF_BATCH_PER_START, qf.QF_BATCH_PAPER])
+def test_numeric_fail_start_both_engines(policy, monkeypatch):
+    """A start whose circuit tensor turns non-finite (fault injection,
+    QF_DEBUG_POISON) fails alone: NUMERIC_FAIL after its first sweep, with the
+    Delta and sweep count of that sweep, on the resident engine (cooperative
+    batch launch) and on the streaming engine alike; the other starts are
+    untouched (same results as the call without the fault)."""
+    w = qfgen.workload("C3+")
+    c = qf.Circuit.from_workload(w)
+    V, init = w.target_unitary(), w.initial(0, 24)
+    kw = dict(batch_policy=policy, max_iters=30)
+    clean = qf.qf_instantiate(c, V, init, **kw)
+    monkeypatch.setenv("QF_DEBUG_POISON", "5")
+    res = qf.qf_instantiate(c, V, init, **kw)
+    monkeypatch.setenv("QF_RES_BATCH", "0")
+    stream = qf.qf_instantiate(c, V, init, engine=qf.QF_ENGINE_STREAM, **kw)
+    for r in (res, stream):
+        assert r.verdict[5] == qf.QF_NUMERIC_FAIL and r.iters[5] == 1, (r.verdict[5], r.iters[5])
+        assert not np.isfinite(r.delta[5])
+    assert np.array_equal(res.verdict, stream.verdict) and np.array_equal(res.iters, stream.iters)
+    others = np.arange(24) != 5
+    if policy == qf.QF_BATCH_PER_START:
+        assert np.array_equal(res.summary[others], clean.summary[others])
+    else:  # a failed start does not hold or stop the batch
+        assert np.array_equal(res.verdict[others], clean.verdict[others])
+        assert np.array_equal(res.iters[others], clean.iters[others])
