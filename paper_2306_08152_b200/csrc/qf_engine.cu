@@ -48,9 +48,19 @@ int resident_threads(int n, int maxm) { return resident_wide(n, maxm) ? 256 : re
 
 // dynamic shared memory of k_resident: the tensor, 8 operand slots (16 complex
 // each for WIDE, else 64), two MMA tile tables and (WIDE) the 16 x 16 T
-size_t resident_smem(int N, bool wide) {
+size_t resident_smem(int N, bool wide, int gcache = 0) {
   return (size_t)N * N * 16 + 8 * (wide ? 16 : 64) * 16 + kResTabBytes +
-         (wide ? 256 * 16 + ((sizeof(WDesc) + 15) & ~size_t(15)) : 0);
+         (wide ? 256 * 16 + ((sizeof(WDesc) + 15) & ~size_t(15)) : (size_t)gcache * 16);
+}
+
+// SMALL resident kernels (n <= 4) keep a start's gates and the CONSTANT
+// matrices in shared memory when they fit this many complex entries
+// (QF_GCACHE=0 disables; A/B)
+constexpr int kGateCacheMax = 1536;  // 24 KiB
+int gate_cache_size(int n, long long gstride, long long ncm) {
+  const char *e = getenv("QF_GCACHE");
+  if (n > 4 || (e && atoi(e) == 0) || gstride + ncm > kGateCacheMax) return 0;
+  return (int)(gstride + ncm);
 }
 
 // CUDA-event timing of individual launches (qf_params.profile = 1): a ring of
@@ -1300,7 +1310,8 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
     const auto kern = resident_kernel(c.n, maxm);
-    const size_t smem = resident_smem(N, resident_wide(c.n, maxm));
+    const size_t smem = resident_smem(N, resident_wide(c.n, maxm),
+                                      gate_cache_size(c.n, c.var_doubles / 2, (long long)c.const_mats.size() / 2));
     int per_sm = 0;
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, resident_threads(c.n, maxm), smem));
@@ -1375,7 +1386,9 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     int maxm = 1;
     for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
     const int threads = resident_threads(c.n, maxm);
-    const size_t smem = resident_smem(N, resident_wide(c.n, maxm));
+    A.ncm = (int)(c.const_mats.size() / 2);
+    A.gcache = gate_cache_size(c.n, c.var_doubles / 2, A.ncm);
+    const size_t smem = resident_smem(N, resident_wide(c.n, maxm), A.gcache);
     auto kern = resident_kernel(c.n, maxm);
     QF_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -1792,6 +1805,7 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
     P.var_doubles = c.var_doubles;
     P.gstride = c.var_doubles / 2;
     P.gd = reinterpret_cast<const GateDesc *>(W + off[q].gd);
+    P.ncm = (int)(c.const_mats.size() / 2);
     P.wdt = reinterpret_cast<const WDesc *>(W + off[q].wdt);
     P.vdag = reinterpret_cast<const double2 *>(W + off[q].vdag);
     P.cmats = reinterpret_cast<const double2 *>(W + off[q].cm);
@@ -1848,8 +1862,17 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
   for (int q = 0; q < np; q++) minn = std::min(minn, cs[q]->n);
   const bool wide = resident_wide(minn, maxm) && resident_wide(maxn, maxm);
   const int threads = wide ? 256 : resident_threads(maxn);
-  const size_t smem = resident_smem(A.N, wide);
   const bool small = maxn <= 4;
+  // SMALL: gate cache sized for the largest problem (0 if any does not fit)
+  int gc = small ? 1 : 0;
+  for (int q = 0; q < np && gc; q++) {
+    const int need = gate_cache_size(cs[q]->n, cs[q]->var_doubles / 2,
+                                     (long long)cs[q]->const_mats.size() / 2);
+    gc = need > 0 || (cs[q]->var_doubles == 0 && cs[q]->const_mats.empty()) ? std::max(gc, need) : 0;
+  }
+  A.gcache = gc;
+  A.ncm = 0;
+  const size_t smem = resident_smem(A.N, wide, A.gcache);
   auto kern = wide ? k_resident<4, true, false, true>
               : small ? (maxm == 1 ? k_resident<2, true, true> : maxm == 2 ? k_resident<4, true, true>
                                                                            : k_resident<8, true, true>)

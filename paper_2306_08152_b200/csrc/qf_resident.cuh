@@ -53,6 +53,7 @@ struct ResProb {
   const double2 *cmats;  // CONSTANT gate matrices
   double2 *gates;        // S x gstride: packed VARIABLE gates
   const struct WDesc *wdt;  // WIDE: 2p transitions (host-built)
+  int ncm;               // complex entries of cmats (SMALL gate cache)
 };
 
 // What a CTA needs of the problem of the start it runs (uniform values)
@@ -82,6 +83,11 @@ struct ResidentArgs {
   int sw_ilp;         // WIDE: MMA tiles in flight per sandwich warp while warp 0 prepares
   int ovl;            // WIDE: overlap the next step's environment + polar with the sandwich
   int poison;         // >= 0: this start's tensor is set non-finite after init (tests only)
+  // SMALL: a start's packed gates and the CONSTANT matrices live in shared
+  // memory for the whole run (the per-step u_old load and u_new store then
+  // stay on chip -- the steps of n <= 4 are latency-bound); gcache = complex
+  // capacity of that region (0: off), ncm = complex entries of cmats
+  int gcache, ncm;
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
   // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
@@ -373,6 +379,7 @@ __device__ void res_gather_d(const ResidentArgs &A, const ResView &V, const doub
   // threads per output: a power of two in [1, 32] (shifts, no runtime division)
   int ltpo = (31 - __clz(nt)) - 2 * LD;
   ltpo = ltpo < 0 ? 0 : (ltpo > A.gather_ltpo_max ? A.gather_ltpo_max : ltpo);
+  ltpo = ltpo > V.n - LD ? V.n - LD : ltpo;  // no more threads per output than rests
   const int tpo = 1 << ltpo;
   const int groups = nt >> ltpo;
   const int k = threadIdx.x & (tpo - 1);
@@ -538,7 +545,9 @@ __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const 
   const int nb = V.N / g.d;
   const bool blocks = !SMALL && nb * nb >= nt;
   if (g.d == 2) {
-    if (blocks) res_sandwich_blocks<2, WIDE>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
+    // 2 x 2 register blocks (8 registers) also in SMALL launches: one
+    // barrier-free pass instead of two phases (n = 2: 956 -> ~300 cycles)
+    if (blocks || SMALL) res_sandwich_blocks<2, WIDE>(ct, g, V.n, V.N, Lb, Rb, t0, nt);
     else res_sandwich<2, WIDE>(ct, g, V.n, V.N, Lb, Rb);
   } else if constexpr (MAXD >= 4) {
     if (g.d == 4) {
@@ -830,6 +839,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
   int *tabs = reinterpret_cast<int *>(Vm + SL);  // [2][128] d = 4 MMA tile addresses (n <= 6)
   double2 *Tm = reinterpret_cast<double2 *>(tabs + 256);  // WIDE: T (<= 16 x 16)
   WDesc *wd = reinterpret_cast<WDesc *>(Tm + 256);        // WIDE: transition in W space
+  double2 *gcache = reinterpret_cast<double2 *>(tabs + 256);  // SMALL: gates + CONSTANT matrices
   const GateDesc *gdesc = A.gd;  // kernel parameters (constant bank); MULTI: per problem
   __shared__ int s_start, s_verdict;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -847,6 +857,8 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
     const int s = s_start;
     if (s >= A.S) break;
     ResView V;
+    long long gstride_cur = A.gstride;
+    int ncm_cur = A.ncm;
     if constexpr (MULTI) {
       int lo = 0, hi = A.nprob - 1;  // last problem with start0 <= s
       while (lo < hi) {
@@ -862,6 +874,8 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       V.cmats = P.cmats;
       V.u0 = P.gates + (long long)(s - P.start0) * P.gstride;
       V.wdt = P.wdt;
+      gstride_cur = P.gstride;
+      ncm_cur = P.ncm;
       gdesc = P.gd;  // global memory
     } else {
       V.n = A.n;
@@ -871,6 +885,18 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       V.cmats = A.cmats;
       V.u0 = A.gates + (long long)s * A.gstride;
       V.wdt = A.wdt;
+    }
+    double2 *const u_global = V.u0;
+    int gcount = 0;  // complex entries of this start's packed gates (SMALL cache)
+    if constexpr (SMALL) {
+      if (A.gcache > 0) {
+        gcount = (int)gstride_cur;
+        for (int e = tid; e < gcount; e += nt) gcache[e] = V.u0[e];
+        for (int e = tid; e < ncm_cur; e += nt) gcache[gcount + e] = V.cmats[e];
+        __syncthreads();
+        V.u0 = gcache;
+        V.cmats = gcache + gcount;
+      }
     }
     const int steps = 2 * V.p;
     auto gate_of = [&](int j, int &fw) {
@@ -1180,6 +1206,12 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       }
     }
     __syncthreads();
+    if constexpr (SMALL) {  // the cached gates back to global memory
+      if (V.u0 != u_global) {
+        for (int e = tid; e < gcount; e += nt) u_global[e] = V.u0[e];
+        __syncthreads();
+      }
+    }
   }
 }
 
