@@ -687,13 +687,20 @@ struct Engine {
     else if (grp_next_w > 0 && A.tiles_per_start <= L.max_parts) {
       // grouped steps: T of the next group (its W as a pseudo-gate)
       const Bits nb = make_bits_loc(c.n, grp_next_wq, grp_next_w);
-      A.nx_env = 1;
       A.nd = nb.d;
       A.nmask = nb.abits[nb.d - 1];
       for (int a = 0; a < nb.d; a++) A.nab[a] = nb.abits[a];
       A.part = reinterpret_cast<double2 *>(ws + L.part);
       A.part_stride = (long long)L.max_parts * 64;
       grp_part_tiles = A.tiles_per_start;
+      // mode 2: the producer warp copies the needed elements per tile row
+      // (no consumer epilogue) when rows x d' fits the 64-entry per-tile slot
+      const bool rowvals = group_fuse == 2 && A.RT * D * nb.d <= 64 &&
+                           A.tiles_per_start * A.RT * D <= kRowListMax;
+      A.nx_env = rowvals ? 2 : 1;
+      grp_part_mode = rowvals ? 2 : 1;
+      grp_part_bits = A.b;
+      grp_part_rt = A.RT;
     }
     if (next_trace) {
       A.nx_trace = 1;
@@ -725,9 +732,16 @@ struct Engine {
   // grouped steps: W of the next group (the flush epilogue's pseudo-gate) and
   // the tiles of the partials it left (0 = none: the next group gathers)
   int grp_next_w = 0, grp_next_wq[3] = {0, 0, 0}, grp_part_tiles = 0;
-  // measured 5.6 % slower at C5 (3 sweeps 3917 -> 4137 ms, same box): the
-  // 64-entry epilogue on every flush tile costs more than the gather it saves
-  int group_fuse = getenv("QF_GROUP_FUSE") ? atoi(getenv("QF_GROUP_FUSE")) : 0;
+  int grp_part_mode = 1, grp_part_rt = 1;  // layout of the partials (RowTileArgs nx_env)
+  Bits grp_part_bits{};
+  // how the next group gets T when its flush runs on the row-tile kernel:
+  // 0 = k_group's strided gather (4x DRAM amplification); 1 = a consumer
+  // epilogue sums tile partials (5.6-11 % slower flushes: it stalls the
+  // consumers before the slot goes back to the producer); 2 (default) = the
+  // producer warp copies the needed elements of each retired row and k_group
+  // sums them in a host-built fixed order (C5 init + 2 sweeps: environment
+  // kernels 153 -> 87 ms, flushes +16 ms, -1.8 % overall)
+  int group_fuse = getenv("QF_GROUP_FUSE") ? atoi(getenv("QF_GROUP_FUSE")) : 2;
   bool next_trace = false;
   // fused partials available for env(part_k, part_dir) / the trace
   int part_k = -1, part_dir = 0, part_tiles = 0, tpart_tiles = 0;
@@ -910,6 +924,29 @@ struct Engine {
       A.part = reinterpret_cast<const double2 *>(ws + L.part);
       A.part_stride = (long long)L.max_parts * 64;
       A.part_tiles = ptiles;
+      A.part_mode = grp_part_mode;
+      if (grp_part_mode == 2) {  // the flush rows of each T row, fixed order
+        const Bits bw = make_bits_loc(c.n, G.wq.data(), w);
+        const Bits &bf = grp_part_bits;
+        const int rows = grp_part_rt * bf.d, nmask = bw.abits[bw.d - 1];
+        std::vector<std::vector<int>> lists(bw.d);
+        for (int t = 0; t < ptiles; t++)
+          for (int q = 0; q < rows; q++) {
+            const int r = t * grp_part_rt + q / bf.d;
+            int i = bf.abits[q % bf.d];
+            for (int u = 0; u < c.n - bf.m; u++)
+              if ((r >> u) & 1) i |= 1 << bf.rest_pos[u];
+            const int ap = i & nmask;
+            for (int a = 0; a < bw.d; a++)
+              if (bw.abits[a] == ap) lists[a].push_back(t * rows + q);
+          }
+        int e = 0;
+        for (int a = 0; a < bw.d; a++) {
+          A.rl_begin[a] = e;
+          for (int off : lists[a]) A.rowlist[e++] = (unsigned short)off;
+        }
+        A.rl_begin[bw.d] = e;
+      }
     }
     A.bw = make_bits_loc(c.n, G.wq.data(), w);
     A.N = N;

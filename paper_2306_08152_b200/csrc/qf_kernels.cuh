@@ -1195,6 +1195,11 @@ struct RowTileArgs {
   //   part[s][tile][a'*d'+b'] = sum_{tile rows i, i&nmask == nab[a']}
   //                             ct[i][(i & ~nmask) | nab[b']]
   // and/or the partial trace tpart[s][tile] = sum_{tile rows i} ct[i][i].
+  // nx_env = 2 (grouped steps): no consumer epilogue; when the producer
+  // retires a tile, lane q (a tile row, global row i) also copies the d'
+  // elements the next group's T needs from that row,
+  //   part[s][tile][q][b'] = ct[i][(i & ~nmask) | nab[b']],
+  // and k_group sums them (rows and tiles in a fixed order, GroupArgs rowlist)
   int nx_env, nd, nmask;
   int nab[8];
   double2 *part;
@@ -1279,6 +1284,18 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
         ptx::mbar_wait(&computed[st], (uint32_t)((jr / A.stages) & 1));
         int s, tt;
         tile_of(jr, s, tt);
+        if (A.nx_env == 2 && lane < rows) {  // the next group's T entries of row `lane`
+          const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
+          const double2 *src = tiles + (size_t)st * tile_elems + rowp(lane) + (row & ~A.nmask);
+          double2 *dst = A.part + (long long)s * A.part_stride + ((long long)tt * rows + lane) * A.nd;
+          double2 v[8];
+#pragma unroll
+          for (int b = 0; b < 8; b++)
+            if (b < A.nd) v[b] = src[A.nab[b]];
+#pragma unroll
+          for (int b = 0; b < 8; b++)
+            if (b < A.nd) dst[b] = v[b];
+        }
         if (lane < rows) {
           const int row = spread_rest(A.b, tt * A.RT + lane / D) | myrow;
           ptx::bulk_s2g(A.ct + (long long)s * A.ct_stride + (long long)row * N,
@@ -1547,7 +1564,7 @@ __global__ void __launch_bounds__(kRowThreads + 32, MINB) k_sandwich_rows(const 
 #endif
     // fused epilogue: partial environment / trace of the next step (fixed
     // order over the tile's rows => independent of batch and sharding)
-    if (A.nx_env) {
+    if (A.nx_env == 1) {
       const int dd2 = A.nd * A.nd;
       for (int o = tid; o < dd2; o += kRowThreads) {
         const int ap = A.nab[o / A.nd], bp = A.nab[o % A.nd];
@@ -1700,6 +1717,8 @@ struct GroupStep {
   int gab[8];   // W-local index of gate-local index a
 };
 
+constexpr int kRowListMax = 512;  // tiles x rows of a flush (= N / RT * RT <= 512, n <= 9)
+
 struct GroupArgs {
   Bits bw;  // W as a pseudo-gate (T gather, flush)
   int N;
@@ -1719,6 +1738,12 @@ struct GroupArgs {
   const double2 *part;
   long long part_stride;
   int part_tiles;
+  // part_mode 2: per-row values of the flush (RowTileArgs nx_env = 2);
+  // rowlist[rl_begin[a'] .. rl_begin[a' + 1]) = offsets tile * rows + q of the
+  // flush rows whose pattern on W is nab[a'], ascending
+  int part_mode;
+  int rl_begin[9];
+  unsigned short rowlist[kRowListMax];
   int nsteps;
   GroupStep st[kGroupMax];
 };
@@ -1733,6 +1758,46 @@ __device__ __forceinline__ void group_mm(const double2 *Am, const double2 *Bm, d
 #pragma unroll
     for (int k = 0; k < DW; k++) acc = cfma(Am[r * DW + k], Bm[k * DW + c], acc);
     Cm[o] = acc;
+  }
+  __syncwarp();
+}
+
+// T of grouped steps from the flush's per-row values (GroupArgs part_mode 2,
+// RowTileArgs nx_env = 2): pp[tile][q][b'] holds ct[i][(i & ~nmask) | nab[b']]
+// for tile row q (global row i).  T[a'][b'] sums the rows with
+// (i & nmask) == nab[a'] in the fixed order of the host-built list
+// rowlist[rl_begin[a'] ..) of their offsets tile * rows + q (tiles, then rows,
+// ascending).  One warp; a lane's outputs read 16-byte entries that 8 lanes
+// (the d' columns b') take from the same contiguous row.
+template <int DW>
+__device__ __forceinline__ void warp_sum_rowparts(const GroupArgs &A, const unsigned short *rl,
+                                                  const double2 *pp, int lane, double2 *T) {
+  constexpr int DD = DW * DW, OPL = DD >= 32 ? DD / 32 : 1;
+#pragma unroll
+  for (int h = 0; h < OPL; h++) {
+    const int o = lane + 32 * h;
+    if (o < DD) {
+      const int a = o / DW, b = o % DW;
+      const int e0 = A.rl_begin[a], e1 = A.rl_begin[a + 1];
+      double2 acc = make_double2(0.0, 0.0);
+      int e = e0;
+      for (; e + 8 <= e1; e += 8) {  // 8 loads in flight, added in list order
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = pp[(long long)rl[e + u] * DW + b];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+        }
+      }
+      for (; e < e1; e++) {
+        const double2 v = pp[(long long)rl[e] * DW + b];
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      T[o] = acc;
+    }
   }
   __syncwarp();
 }
@@ -1752,9 +1817,18 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
   double2 *Vm = Am + 64;
   const int nact = *A.n_active;
   const int N = A.N;
+  __shared__ unsigned short rls[kRowListMax];  // part_mode 2: the row lists, block-shared
+  if (A.part && A.part_mode == 2) {
+    for (int e = threadIdx.x; e < A.rl_begin[DW]; e += blockDim.x) rls[e] = A.rowlist[e];
+    __syncthreads();
+  }
   for (int ai = blockIdx.x * kEnvWarps + w; ai < nact; ai += gridDim.x * kEnvWarps) {
     const int s = A.active[ai];
-    if (A.part) {
+    if (A.part && A.part_mode == 2) {
+      // T from the flush's per-row values: T[a'][b'] = sum over tiles, then
+      // tile rows (ascending), of the rows whose pattern on W is nab[a']
+      warp_sum_rowparts<DW>(A, rls, A.part + (long long)s * A.part_stride, lane, T);
+    } else if (A.part) {
       // T = sum over the flushing sandwich's tiles, tile order
       warp_sum_parts<DW>(A.part + (long long)s * A.part_stride, A.part_tiles, lane, T);
     } else {
