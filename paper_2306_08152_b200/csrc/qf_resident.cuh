@@ -88,6 +88,7 @@ struct ResidentArgs {
   // stay on chip -- the steps of n <= 4 are latency-bound); gcache = complex
   // capacity of that region (0: off), ncm = complex entries of cmats
   int gcache, ncm;
+  int gather_warp;    // 1: the serial warp gathers the environment itself (no barrier)
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
   // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
@@ -415,6 +416,61 @@ __device__ __forceinline__ void res_gather(const ResidentArgs &A, const ResView 
       res_gather_d<4, WS>(A, V, ct, g, Pm);
     } else if constexpr (MAXD >= 8) {
       res_gather_d<8, WS>(A, V, ct, g, Pm);
+    }
+  }
+}
+
+// The same environment on one warp (the serial warp, right before its
+// update): SPLIT lanes per output take r = k, k + SPLIT, ... ascending, a
+// fixed xor tree combines them; every lane's loads are issued together.
+// Saves the CTA barrier between an all-thread gather and the update.
+template <int D, bool WS>
+__device__ __forceinline__ void res_gather_warp_d(const ResView &V, const double2 *ct,
+                                                  const GateDesc &g, double2 *Pm, int lane) {
+  constexpr int DD = D * D, SPLIT = DD >= 32 ? 1 : 32 / DD, OPL = DD >= 32 ? DD / 32 : 1;
+  constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
+  const int R = V.N >> LD, k = lane % SPLIT;
+  double2 acc[OPL];
+  int ia[OPL], ib[OPL];
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+    const int o = lane / SPLIT + q * (32 / SPLIT);
+    ia[q] = g.abits[o / D];
+    ib[q] = g.abits[o % D];
+    acc[q] = make_double2(0.0, 0.0);
+  }
+#pragma unroll 4
+  for (int r = k; r < R; r += SPLIT) {
+    const int sp = rspread(g, V.n, r);
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {
+      const double2 v = ct[sidxw<WS>(sp | ia[q], sp | ib[q], V.N)];
+      acc[q].x += v.x;
+      acc[q].y += v.y;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < OPL; q++) {
+#pragma unroll
+    for (int off = 1; off < SPLIT; off <<= 1) {
+      acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, off);
+      acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, off);
+    }
+    if (k == 0) Pm[lane / SPLIT + q * (32 / SPLIT)] = acc[q];
+  }
+  __syncwarp();
+}
+
+template <int MAXD, bool WS = false>
+__device__ __forceinline__ void res_gather_warp(const ResView &V, const double2 *ct,
+                                                const GateDesc &g, double2 *Pm, int lane) {
+  if (g.d == 2) {
+    res_gather_warp_d<2, WS>(V, ct, g, Pm, lane);
+  } else if constexpr (MAXD >= 4) {
+    if (g.d == 4) {
+      res_gather_warp_d<4, WS>(V, ct, g, Pm, lane);
+    } else if constexpr (MAXD >= 8) {
+      res_gather_warp_d<8, WS>(V, ct, g, Pm, lane);
     }
   }
 }
@@ -920,7 +976,19 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       const int off = (j2 & 1) * SL;
       if (res_use_dmma4<MAXD, SMALL, WIDE>(g2, V))
         res_dmma4_table(g2, V.n, V.N, tabs + (j2 & 1) * 128);  // barriers follow
-      if (g2.kind != 1) {
+      if (g2.kind != 1 && A.gather_warp) {
+        // the serial warp gathers its own environment: no CTA barrier before
+        // the update
+        if (serial) {
+          const double2 *u2 = V.u0 + g2.goff;
+#pragma unroll
+          for (int q = 0; q < 2; q++) {
+            const int e = lane + 32 * q;
+            if (e < g2.d * g2.d) Uo[e] = pre ? upf[q] : u2[e];
+          }
+          res_gather_warp<MAXD, WIDE>(V, ct, g2, Pm, lane);
+        }
+      } else if (g2.kind != 1) {
 #ifdef QF_POLAR_COUNT
         const long long tg0 = clock64();
 #endif
