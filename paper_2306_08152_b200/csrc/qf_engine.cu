@@ -22,6 +22,7 @@
 #include "qf_internal.h"
 #include "qf_kernels.cuh"
 #include "qf_resident.cuh"
+#include "qf_lean.cuh"
 
 namespace qf {
 
@@ -36,6 +37,16 @@ int resident_threads(int n) {
   // 128 threads keep 3 CTAs (= 3 resident 64 KiB tensors at n = 6) per SM
   const int items = (1 << (2 * n)) / 4;
   return std::max(32, std::min(128, items));
+}
+
+// k_lean (one warp per start, compile-time tensor size) for n <= 3 with gates
+// of at most 2 qubits and the per-start policy; QF_LEAN=0 keeps k_resident
+// (A/B, and the tests comparing single calls with multi-problem launches
+// bitwise)
+bool lean_ok(const qf_circuit_s &c, int maxm, bool warm) {
+  const char *e = getenv("QF_LEAN");
+  return !(e && atoi(e) == 0) && c.n <= 3 && maxm <= 2 && !warm &&
+         (long long)c.var_doubles / 2 + (long long)c.const_mats.size() / 2 <= 4096;
 }
 
 // the WIDE resident variant (256 threads, FP64-MMA d = 4 sandwich): n = 5, 6
@@ -1447,6 +1458,15 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       void *args[] = {&A};
       QF_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(g),
                                            dim3(threads), args, smem, st));
+    } else if (lean_ok(c, maxm, E.warm)) {
+      // n <= 3, gates <= 2 qubits: one warp per start (k_lean)
+      const size_t lsm = ((size_t)kLeanFixed + A.gstride + A.ncm) * 16;
+      auto lk = c.n == 1 ? k_lean<1> : c.n == 2 ? k_lean<2> : k_lean<3>;
+      QF_CHECK(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+      int lper = 0;
+      QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lper, lk, 32, lsm));
+      const int lg = std::max(1, std::min(S, std::max(1, lper) * E.nsm));
+      lk<<<lg, 32, lsm, st>>>(A);
     } else {
       kern<<<g, threads, smem, st>>>(A);
     }
@@ -2050,6 +2070,7 @@ extern "C" void qf_debug_polar_counts(unsigned long long *out) {
   cudaMemcpyFromSymbol(&out[8], qf::qf_t_polar, 8);
   cudaMemcpyFromSymbol(&out[9], qf::qf_n_upd, 8);
   cudaMemcpyFromSymbol(&out[10], qf::qf_t_ovl, 32);
+  cudaMemcpyFromSymbol(&out[14], qf::qf_t_lean, 48);
 }
 // row-tile d = 8 phase timers: wait-for-data, phase 1, phase 2, epilogue, tiles
 extern "C" void qf_debug_rows_counts(unsigned long long *out) {

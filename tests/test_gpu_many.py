@@ -65,6 +65,7 @@ def test_many_mixed_against_single_and_oracle(monkeypatch):
     # references take the same kernel (QF_RES_WIDE=0: no 256-thread variant
     # for the n = 5 problem), so verdicts and sweep counts must match exactly
     monkeypatch.setenv("QF_RES_WIDE", "0")
+    monkeypatch.setenv("QF_LEAN", "0")  # nor the one-warp kernel for the n <= 3 problems
     probs, Vs, inits = [], [], []
     for name, S in (("C1", 4), ("C2+", 16), ("C3+", 48)):
         w = qfgen.workload(name)
@@ -92,8 +93,9 @@ def test_many_mixed_against_single_and_oracle(monkeypatch):
         assert np.abs(got[q].gates[same] - o.gates[same]).max() < 1e-10, q
 
 
-def test_many_degenerate():
+def test_many_degenerate(monkeypatch):
     """A problem with zero starts and a constant-only circuit ride along."""
+    monkeypatch.setenv("QF_LEAN", "0")  # the reference call on k_resident, as the launch
     w = qfgen.workload("C2+")
     pr = (w.n, w.locs, w.kinds, w.const_mats)
     cx = np.eye(4)[[0, 1, 3, 2]]

@@ -26,7 +26,7 @@ eng = {"stream": 1, "resident": 2}.get(sys.argv[3] if len(sys.argv) > 3 else "au
 w = qfgen.workload(name)
 c = qf.Circuit.from_workload(w)
 r = qf.qf_instantiate(c, w.target_unitary(), w.initial(), max_iters=iters, engine=eng)
-out = (ctypes.c_ulonglong * 14)()
+out = (ctypes.c_ulonglong * 20)()
 qf.lib().qf_debug_polar_counts(out)
 print(f"{name} {iters} sweeps: NS calls {out[0]}, NS iterations {out[1]} "
       f"({out[1] / max(1, out[0]):.2f} per call), Jacobi sweeps {out[2]}")
@@ -43,6 +43,11 @@ if out[13]:
           f"{out[12] / out[13]:.0f} cycles ({out[13]} steps)")
     print(f"  phase A per step: warp 0 {out[3] / out[5]:.0f}, warp 1 (sandwich) {out[4] / out[5]:.0f}; "
           f"after the barrier (tile table + T gather) {out[6] / out[5]:.0f} cycles")
+
+if out[19]:
+    nl = out[19]
+    print(f"  k_lean per step: sandwich {out[14] / nl:.0f}, env {out[15] / nl:.0f}, form A {out[16] / nl:.0f}, "
+          f"polar {out[17] / nl:.0f}, L/R {out[18] / nl:.0f} cycles ({nl} steps)")
 
 rc = (ctypes.c_ulonglong * 5)()
 qf.lib().qf_debug_rows_counts(rc)
