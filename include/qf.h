@@ -167,6 +167,9 @@ typedef struct {
   double resident_ms;       /* k_resident CUDA-event time (profile = 1)    */
   double sweep_flops;       /* algorithmic flops of all gate applications: */
                             /* 16 d N^2 per step, 8 d N^2 per init pass    */
+  int32_t resident_kernel;  /* resident engine kernel: 0 k_resident, 1 its  */
+                            /* WIDE variant, 2 k_lean, 3 k_reg; -1 streaming*/
+  int32_t reserved;
 } qf_stats;
 
 void qf_params_default(qf_params *p);

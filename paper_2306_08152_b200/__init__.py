@@ -101,6 +101,8 @@ class qf_stats(ctypes.Structure):
         ("env_ms", ctypes.c_double),
         ("resident_ms", ctypes.c_double),
         ("sweep_flops", ctypes.c_double),
+        ("resident_kernel", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -23,6 +23,7 @@
 #include "qf_kernels.cuh"
 #include "qf_resident.cuh"
 #include "qf_lean.cuh"
+#include "qf_reg.cuh"
 
 namespace qf {
 
@@ -47,6 +48,19 @@ bool lean_ok(const qf_circuit_s &c, int maxm, bool warm) {
   const char *e = getenv("QF_LEAN");
   return !(e && atoi(e) == 0) && c.n <= 3 && maxm <= 2 && !warm &&
          (long long)c.var_doubles / 2 + (long long)c.const_mats.size() / 2 <= 4096;
+}
+
+// k_reg (the tensor in the warp's registers) where lean_ok holds and every
+// VARIABLE gate is one-qubit (closed-form polar factor), no R_z gates;
+// QF_REG=0 keeps k_lean (A/B, and the bitwise k_reg == k_lean tests)
+bool reg_ok(const qf_circuit_s &c) {
+  const char *e = getenv("QF_REG");
+  if (e && atoi(e) == 0) return false;
+  for (int k = 0; k < c.p; k++) {
+    if (c.kind[k] == QF_GATE_RZ) return false;
+    if (c.kind[k] == QF_GATE_VARIABLE && c.arity[k] != 1) return false;
+  }
+  return true;
 }
 
 // the WIDE resident variant (256 threads, FP64-MMA d = 4 sandwich): n = 5, 6
@@ -545,6 +559,7 @@ struct Engine {
   bool polar_jacobi = false;  // QF_POLAR=jacobi: Jacobi polar instead of Newton-Schulz
   std::vector<int> voff; // per gate: complex offset of its backward slot in vstore
   long long launches = 0;
+  int res_kernel = -1;  // qf_stats.resident_kernel
   int sandwich_grid[4] = {0, 0, 0, 0};
   // byte accounting: launches per "context" j; the active count in context j
   // is n_active after sweep j (context 0 = the initial S)
@@ -1459,17 +1474,22 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       QF_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(g),
                                            dim3(threads), args, smem, st));
     } else if (lean_ok(c, maxm, E.warm)) {
-      // n <= 3, gates <= 2 qubits: one warp per start (k_lean)
-      const size_t lsm = ((size_t)kLeanFixed + A.gstride + A.ncm) * 16;
-      auto lk = c.n == 1 ? k_lean<1> : c.n == 2 ? k_lean<2> : k_lean<3>;
+      // n <= 3, gates <= 2 qubits: one warp per start (k_reg: tensor in
+      // registers, one-qubit VARIABLE gates; else k_lean: in shared memory)
+      const bool rg = reg_ok(c);
+      const size_t lsm = ((size_t)(rg ? 0 : kLeanFixed) + A.gstride + A.ncm) * 16;
+      auto lk = rg ? (c.n == 1 ? k_reg<1> : c.n == 2 ? k_reg<2> : k_reg<3>)
+                   : (c.n == 1 ? k_lean<1> : c.n == 2 ? k_lean<2> : k_lean<3>);
       QF_CHECK(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
       int lper = 0;
       QF_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lper, lk, 32, lsm));
       const int lg = std::max(1, std::min(S, std::max(1, lper) * E.nsm));
       lk<<<lg, 32, lsm, st>>>(A);
+      E.res_kernel = rg ? 3 : 2;
     } else {
       kern<<<g, threads, smem, st>>>(A);
     }
+    if (E.res_kernel < 0) E.res_kernel = resident_wide(c.n, maxm) ? 1 : 0;
     if (slot >= 0) E.prof.close(slot, st);
     E.launches++;
     QF_CHECK(cudaGetLastError());
@@ -1711,6 +1731,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     r.stats.kernel_launches = E.launches;
     r.stats.sweeps = mx;
     r.stats.engine = resident ? QF_ENGINE_RESIDENT : QF_ENGINE_STREAM;
+    r.stats.resident_kernel = resident ? E.res_kernel : -1;
     r.stats.resident_ms = E.prof.ms[2];
     {
       double step_f = 0.0, init_f = 0.0;
@@ -2015,6 +2036,7 @@ qf_status engine_run_many(int np, const qf_circuit_s *const *cs, const double *c
     r.stats.kernel_launches = launches;
     r.stats.sweeps = mx;
     r.stats.engine = QF_ENGINE_RESIDENT;
+    r.stats.resident_kernel = wide ? 1 : 0;
     r.stats.start_sweeps = ss;
     r.stats.sweep_flops = f;
     r.stats.resident_ms = res_ms;  // the whole launch (shared by its problems)
