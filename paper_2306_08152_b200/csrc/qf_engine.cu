@@ -97,19 +97,17 @@ struct Profiler {
   int kind[kRing] = {};
   int next = 0, used = 0;
   double ms[3] = {0.0, 0.0, 0.0};
+  // events are created on first use of a ring slot (a resident call uses one
+  // pair; creating the whole ring cost ~0.35 ms per call)
   void init() {
-    for (int i = 0; i < kRing; i++) {
-      cudaEventCreate(&beg[i]);
-      cudaEventCreate(&end[i]);
-      kind[i] = -1;
-    }
+    for (int i = 0; i < kRing; i++) kind[i] = -1;
     on = true;
   }
   ~Profiler() {
     if (!on) return;
     for (int i = 0; i < kRing; i++) {
-      cudaEventDestroy(beg[i]);
-      cudaEventDestroy(end[i]);
+      if (beg[i]) cudaEventDestroy(beg[i]);
+      if (end[i]) cudaEventDestroy(end[i]);
     }
   }
   void harvest(int i) {
@@ -124,6 +122,10 @@ struct Profiler {
     const int i = next;
     next = (next + 1) % kRing;
     harvest(i);
+    if (!beg[i]) {
+      cudaEventCreate(&beg[i]);
+      cudaEventCreate(&end[i]);
+    }
     kind[i] = k;
     cudaEventRecord(beg[i], st);
     return i;
@@ -1264,13 +1266,13 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   for (int k = 0; k < c.p; k++)
     if (c.kind[k] != QF_GATE_CONSTANT)  // d < 0: RZ, also check the diag(1, e^{i theta}) form
       tab.push_back(make_int2(c.var_off[k], c.kind[k] == QF_GATE_RZ ? -2 : 1 << c.arity[k]));
-  if (!tab.empty()) {
+  if (!tab.empty() && d_initial != nullptr) {
     QF_CHECK(cudaMemcpyAsync(W + E.L.gtab, tab.data(), tab.size() * sizeof(int2),
                              cudaMemcpyHostToDevice, st));
     h2d += (long long)(tab.size() * sizeof(int2));
   }
-  std::vector<int2> vslots;
-  for (int k = 0; k < c.p; k++)
+  std::vector<int2> vslots;  // warm-start slots (QF_WARM=1 only)
+  for (int k = 0; k < c.p && E.warm; k++)
     if (c.kind[k] != QF_GATE_CONSTANT) {
       const int d = 1 << c.arity[k];
       vslots.push_back(make_int2(E.voff[k], d));
@@ -1351,17 +1353,17 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   } pinned{h_flags, h_cap, h_pinned};
   int *h_nact = h_flags + 1;
   h_nact[0] = S;
-  QF_CHECK(cudaMemcpyAsync(h_flags, E.bad(), sizeof(int), cudaMemcpyDeviceToHost, st));
-  QF_CHECK(cudaStreamSynchronize(st));
-  d2h += 4;
-  if (h_flags[0] & 1) {
-    set_error("target is not unitary to 1e-9 (max-abs of V^dagger V - I)");
-    return QF_E_NOT_UNITARY;
-  }
-  if (h_flags[0] & 2) {
-    set_error("an initial VARIABLE gate is not unitary to 1e-9");
-    return QF_E_NOT_UNITARY;
-  }
+  auto flags_status = [&]() {
+    if (h_flags[0] & 1) {
+      set_error("target is not unitary to 1e-9 (max-abs of V^dagger V - I)");
+      return QF_E_NOT_UNITARY;
+    }
+    if (h_flags[0] & 2) {
+      set_error("an initial VARIABLE gate is not unitary to 1e-9");
+      return QF_E_NOT_UNITARY;
+    }
+    return QF_OK;
+  };
 
   const bool batch = p.batch_policy == QF_BATCH_PAPER;
   // the batch policy runs resident when this call is the whole batch and all
@@ -1383,6 +1385,17 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   const bool resident = p.engine == QF_ENGINE_RESIDENT || resident_batch ||
                         (p.engine == QF_ENGINE_AUTO && !batch && c.n <= kResidentMaxQubits &&
                          c.p <= kResMaxGates);
+  // input checks: the streaming and batch paths read the flags before the
+  // sweeps; the resident kernels read them on the device (a bad input makes
+  // every start return at once) and the host reports them with the results,
+  // so a small instantiation pays no extra host round trip
+  const bool defer_check = resident && !resident_batch;
+  d2h += 4;
+  if (!defer_check) {
+    QF_CHECK(cudaMemcpyAsync(h_flags, E.bad(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    QF_CHECK(cudaStreamSynchronize(st));
+    if (flags_status() != QF_OK) return QF_E_NOT_UNITARY;
+  }
   int last = 0;  // last sweep enqueued (streaming engine)
   cudaEvent_t ev[2];
   QF_CHECK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -1396,14 +1409,17 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   } events{ev};
   if (resident) {
     // ---- a2..a7 in one kernel: one CTA per start, tensor in shared memory
+    // the gate table travels in the kernel parameters; the WIDE variant's
+    // transition descriptors in global memory
     const std::vector<GateDesc> gd = make_gdesc(c, E.warm ? &E.voff : nullptr);
-    QF_CHECK(cudaMemcpyAsync(W + E.L.gdesc, gd.data(), gd.size() * sizeof(GateDesc),
-                             cudaMemcpyHostToDevice, st));
-    h2d += (long long)(gd.size() * sizeof(GateDesc));
-    const std::vector<WDesc> wdt = make_wdescs(gd);
-    QF_CHECK(cudaMemcpyAsync(W + E.L.wdesc, wdt.data(), wdt.size() * sizeof(WDesc),
-                             cudaMemcpyHostToDevice, st));
-    h2d += (long long)(wdt.size() * sizeof(WDesc));
+    int maxm = 1;
+    for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
+    if (resident_wide(c.n, maxm)) {
+      const std::vector<WDesc> wdt = make_wdescs(gd);
+      QF_CHECK(cudaMemcpyAsync(W + E.L.wdesc, wdt.data(), wdt.size() * sizeof(WDesc),
+                               cudaMemcpyHostToDevice, st));
+      h2d += (long long)(wdt.size() * sizeof(WDesc));
+    }
     int *counter = E.n_active() + 2;
     QF_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
     ResidentArgs A{};
@@ -1449,8 +1465,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.rec_cost = reinterpret_cast<double *>(W + E.L.rec_cost);
     A.rec_gates = reinterpret_cast<double *>(W + E.L.rec_gates);
     A.var_doubles = c.var_doubles;
-    int maxm = 1;
-    for (int k = 0; k < c.p; k++) maxm = std::max(maxm, c.arity[k]);
+    A.bad = defer_check ? E.bad() : nullptr;
     const int threads = resident_threads(c.n, maxm);
     A.ncm = (int)(c.const_mats.size() / 2);
     A.gcache = gate_cache_size(c.n, c.var_doubles / 2, A.ncm);
@@ -1478,7 +1493,10 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       // registers, one-qubit VARIABLE gates; else k_lean: in shared memory)
       const bool rg = reg_ok(c);
       const size_t lsm = ((size_t)(rg ? 0 : kLeanFixed) + A.gstride + A.ncm) * 16;
-      auto lk = rg ? (c.n == 1 ? k_reg<1> : c.n == 2 ? k_reg<2> : k_reg<3>)
+      const bool bt = p.beta != 0.0;
+      auto lk = rg ? (c.n == 1 ? (bt ? k_reg<1, true> : k_reg<1, false>)
+                      : c.n == 2 ? (bt ? k_reg<2, true> : k_reg<2, false>)
+                                 : (bt ? k_reg<3, true> : k_reg<3, false>))
                    : (c.n == 1 ? k_lean<1> : c.n == 2 ? k_lean<2> : k_lean<3>);
       QF_CHECK(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
       int lper = 0;
@@ -1679,7 +1697,10 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     QF_CHECK(cudaMemcpyAsync(r.summary.data(), summ, (size_t)S * sizeof(qf_summary),
                              cudaMemcpyDeviceToHost, st));
     QF_CHECK(cudaMemcpyAsync(&best, d_best, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    if (defer_check)
+      QF_CHECK(cudaMemcpyAsync(h_flags, E.bad(), sizeof(int), cudaMemcpyDeviceToHost, st));
     QF_CHECK(cudaStreamSynchronize(st));
+    if (defer_check && flags_status() != QF_OK) return QF_E_NOT_UNITARY;
     d2h += (long long)S * sizeof(qf_summary) + 8;
     r.best = (int)best;
     r.all_gates = out.host_all_gates;
@@ -1756,7 +1777,10 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     r.stats.h2d_bytes += h2d;
     r.stats.d2h_bytes += d2h;
   } else {
+    if (defer_check)
+      QF_CHECK(cudaMemcpyAsync(h_flags, E.bad(), sizeof(int), cudaMemcpyDeviceToHost, st));
     QF_CHECK(cudaStreamSynchronize(st));
+    if (defer_check && flags_status() != QF_OK) return QF_E_NOT_UNITARY;
   }
   return QF_OK;
 }

@@ -38,6 +38,7 @@ __device__ unsigned long long qf_t_lean[8];  // sandwich, env, form A, polar, L/
 
 template <int NQ>
 __global__ void __launch_bounds__(32) k_lean(const __grid_constant__ ResidentArgs A) {
+  if (A.bad != nullptr && *A.bad != 0) return;  // rejected input (host reports it)
   constexpr int N = 1 << NQ, NN = N * N;
   extern __shared__ __align__(16) double2 lsm[];
   double2 *ct = lsm;

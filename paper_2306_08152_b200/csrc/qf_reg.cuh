@@ -52,8 +52,9 @@ __device__ __forceinline__ double2 reg_fetch_u(const double2 (&v)[RegShape<NQ>::
   }
 }
 
-template <int NQ>
+template <int NQ, bool BETA>
 __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs A) {
+  if (A.bad != nullptr && *A.bad != 0) return;  // rejected input (host reports it)
   using RS = RegShape<NQ>;
   constexpr int N = RS::N, EPL = RS::EPL;
   extern __shared__ __align__(16) double2 rsm[];
@@ -117,63 +118,82 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
         left_pass(g, (g.kind != 1 ? gc : cm) + g.goff);
       }
     };
-    // step state produced by prepare(j): the 2 x 2 factors (L: peel / apply
-    // from the left, R: from the right) of a one-qubit gate
-    double2 Lr[4], Rr[4];
-    auto prepare = [&](int j) {
+    // gate step j: environment of the gate from the current ct,
+    // A = E^dagger, the polar factor u_new, then ct <- E(L) ct E(R) (backward
+    // L = u_old^H, R = u_new; forward L = u_new, R = u_old^H).  One straight
+    // block per gate shape, so the sandwich's operand shuffles and (backward)
+    // its left factor overlap the polar factor's dependency chain.
+    auto step = [&](int j) {
       int fw;
       const GateDesc &g = A.gd[gate_of(j, fw)];
-      if (g.d != 2) return;  // CONSTANT 4 x 4: coefficients read by the sandwich
-      double2 Uo[4], Un[4];
-      const double2 *src = (g.kind != 1 ? gc : cm) + g.goff;
+      const int mask = g.mask;
+      double2 out[EPL];
+      if (g.d == 2) {
+        const int m = g.abits[1];
+        const double2 *src = (g.kind != 1 ? gc : cm) + g.goff;
+        double2 Uo[4], Un[4];
 #pragma unroll
-      for (int k = 0; k < 4; k++) Uo[k] = src[k];
-      if (g.kind != 1) {
-        // P[a][b] = sum_r ct[ins(a, r)][ins(b, r)], r ascending (lane: a = bit 1,
-        // b = bit 0 of lane & 3), then every lane takes all four
-        const int m = g.abits[1], b = __ffs(m) - 1;
-        const int ra = ((lane >> 1) & 1) ? m : 0, rc = (lane & 1) ? m : 0;
-        double2 acc = make_double2(0.0, 0.0);
+        for (int k = 0; k < 4; k++) Uo[k] = src[k];
+        // the element's 2 x 2 block, one round of shuffles
+        double2 x[EPL][2][2];
 #pragma unroll
-        for (int r = 0; r < N / 2; r++) {
-          const int rb = ins1(r, b);
-          const double2 x = reg_fetch_any<NQ>(v, (rb | ra) * N + (rb | rc));
-          acc.x += x.x;
-          acc.y += x.y;
+        for (int q = 0; q < EPL; q++) {
+          const int r = eo[q] >> NQ, c = eo[q] & (N - 1);
+          const int rb = r & ~m, cb = c & ~m;
+#pragma unroll
+          for (int a = 0; a < 2; a++) {
+            const int row = rb | (a ? m : 0);
+            const int qs = (m & 4) ? a : q;  // n = 3: row bit 2 is the register index
+#pragma unroll
+            for (int bb = 0; bb < 2; bb++)
+              x[q][a][bb] = reg_fetch_u<NQ>(v, qs, row * N + (cb | (bb ? m : 0)));
+          }
         }
-        double2 P[4];
+        if (g.kind != 1) {
+          // P[a][b] = sum_r ct[ins(a, r)][ins(b, r)], r ascending (lane: a = bit 1,
+          // b = bit 0 of lane & 3), then every lane takes all four
+          const int b = __ffs(m) - 1;
+          const int ra = ((lane >> 1) & 1) ? m : 0, rc = (lane & 1) ? m : 0;
+          double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int k = 0; k < 4; k++) P[k] = shfl2(acc, k);
-        // A = E^dagger with E = (1-beta) PT + beta u_old^dagger (as res_update):
-        // backward A = P^dagger u_old, forward A = u_old P^dagger
-        double2 Am[4];
+          for (int r = 0; r < N / 2; r++) {
+            const int rb = ins1(r, b);
+            const double2 xe = reg_fetch_any<NQ>(v, (rb | ra) * N + (rb | rc));
+            acc.x += xe.x;
+            acc.y += xe.y;
+          }
+          double2 P[4];
 #pragma unroll
-        for (int o = 0; o < 4; o++) {
-          const int r = o >> 1, c = o & 1;
-          double2 a = make_double2(0.0, 0.0);
-          if (!fw) {
+          for (int k = 0; k < 4; k++) P[k] = shfl2(acc, k);
+          // A = E^dagger with E = (1-beta) PT + beta u_old^dagger (as res_update):
+          // backward A = P^dagger u_old, forward A = u_old P^dagger
+          double2 Am[4];
 #pragma unroll
-            for (int k = 0; k < 2; k++) a = cfma_cj(P[k * 2 + r], Uo[k * 2 + c], a);
-          } else {
+          for (int o = 0; o < 4; o++) {
+            const int r = o >> 1, c = o & 1;
+            double2 a = make_double2(0.0, 0.0);
+            if (!fw) {
 #pragma unroll
-            for (int k = 0; k < 2; k++) {
-              const double2 x = Uo[r * 2 + k], pv = P[c * 2 + k];
-              a.x = fma(x.x, pv.x, a.x);
-              a.x = fma(x.y, pv.y, a.x);
-              a.y = fma(x.y, pv.x, a.y);
-              a.y = fma(-x.x, pv.y, a.y);
+              for (int k = 0; k < 2; k++) a = cfma_cj(P[k * 2 + r], Uo[k * 2 + c], a);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 2; k++) {
+                const double2 xu = Uo[r * 2 + k], pv = P[c * 2 + k];
+                a.x = fma(xu.x, pv.x, a.x);
+                a.x = fma(xu.y, pv.y, a.x);
+                a.y = fma(xu.y, pv.x, a.y);
+                a.y = fma(-xu.x, pv.y, a.y);
+              }
             }
+            if constexpr (BETA) {
+              a = cscale(a, 1.0 - A.beta);
+              a.x = fma(A.beta, Uo[o].x, a.x);
+              a.y = fma(A.beta, Uo[o].y, a.y);
+            }
+            Am[o] = a;
           }
-          if (A.beta != 0.0) {
-            a = cscale(a, 1.0 - A.beta);
-            a.x = fma(A.beta, Uo[o].x, a.x);
-            a.y = fma(A.beta, Uo[o].y, a.y);
-          }
-          Am[o] = a;
-        }
-        // closed-form 2 x 2 polar factor (warp_polar_jacobi<2>, every output
-        // on every lane): U = (A + (det/|det|) adj(A)^H) / sqrt(||A||_F^2 + 2|det A|)
-        {
+          // closed-form 2 x 2 polar factor (warp_polar_jacobi<2>, every output
+          // on every lane): U = (A + (det/|det|) adj(A)^H) / sqrt(||A||_F^2 + 2|det A|)
           const double2 a = Am[0], bb = Am[1], c = Am[2], e = Am[3];
           const double2 det = make_double2(a.x * e.x - a.y * e.y - (bb.x * c.x - bb.y * c.y),
                                            a.x * e.y + a.y * e.x - (bb.x * c.y + bb.y * c.x));
@@ -191,53 +211,38 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
             Un[0] = Un[3] = make_double2(1.0, 0.0);
             Un[1] = Un[2] = make_double2(0.0, 0.0);
           }
-        }
-        if (lane < 4) {
-          const double2 w = lane == 0 ? Un[0] : lane == 1 ? Un[1] : lane == 2 ? Un[2] : Un[3];
-          gc[g.goff + lane] = w;  // u_new
-        }
-        __syncwarp();
-      } else {
+          if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < 4; k++) Un[k] = Uo[k];
-      }
-      // backward: L = u_old^H, R = u_new; forward: L = u_new, R = u_old^H
+            for (int k = 0; k < 4; k++) gc[g.goff + k] = Un[k];  // u_new
+          }
+        } else {
 #pragma unroll
-      for (int o = 0; o < 4; o++) {
-        const double2 od = cconj(Uo[(o & 1) * 2 + (o >> 1)]);
-        Lr[o] = fw ? Un[o] : od;
-        Rr[o] = fw ? od : Un[o];
-      }
-    };
-    // step j: ct <- E(L) ct E(R)
-    auto sandwich = [&](int j) {
-      int fw;
-      const GateDesc &g = A.gd[gate_of(j, fw)];
-      const int mask = g.mask;
-      double2 out[EPL];
-      if (g.d == 2) {  // the element's 2 x 2 block in one round of shuffles
-        const int m = g.abits[1];
+          for (int k = 0; k < 4; k++) Un[k] = Uo[k];  // CONSTANT: the fixed matrix
+        }
+        // the lane's coefficients: row i of L, column jj of R
 #pragma unroll
         for (int q = 0; q < EPL; q++) {
           const int r = eo[q] >> NQ, c = eo[q] & (N - 1);
           const int i = (r & m) != 0, jj = (c & m) != 0;
-          const int rb = r & ~m, cb = c & ~m;
-          double2 x[2][2];
-#pragma unroll
-          for (int a = 0; a < 2; a++) {
-            const int row = rb | (a ? m : 0);
-            const int qs = (m & 4) ? a : q;  // n = 3: row bit 2 is the register index
-#pragma unroll
-            for (int bb = 0; bb < 2; bb++) x[a][bb] = reg_fetch_u<NQ>(v, qs, row * N + (cb | (bb ? m : 0)));
+          double2 l0, l1, r0, r1;
+          if (!fw) {
+            l0 = cconj(i ? Uo[1] : Uo[0]);
+            l1 = cconj(i ? Uo[3] : Uo[2]);
+            r0 = jj ? Un[1] : Un[0];
+            r1 = jj ? Un[3] : Un[2];
+          } else {
+            l0 = i ? Un[2] : Un[0];
+            l1 = i ? Un[3] : Un[1];
+            r0 = cconj(jj ? Uo[2] : Uo[0]);
+            r1 = cconj(jj ? Uo[3] : Uo[1]);
           }
-          const double2 l0 = i ? Lr[2] : Lr[0], l1 = i ? Lr[3] : Lr[1];
-          const double2 y0 = cfma(l1, x[1][0], cmul(l0, x[0][0]));
-          const double2 y1 = cfma(l1, x[1][1], cmul(l0, x[0][1]));
-          const double2 r0 = jj ? Rr[1] : Rr[0], r1 = jj ? Rr[3] : Rr[2];
+          const double2 y0 = cfma(l1, x[q][1][0], cmul(l0, x[q][0][0]));
+          const double2 y1 = cfma(l1, x[q][1][1], cmul(l0, x[q][0][1]));
           out[q] = cfma(y1, r1, cmul(y0, r0));
         }
 #pragma unroll
         for (int q = 0; q < EPL; q++) v[q] = out[q];
+        __syncwarp();  // u_new visible to the next step's u_old load
       } else {  // CONSTANT 4 x 4: left pass, then right pass (k_lean pass4)
         const double2 *M = cm + g.goff;
         const int a1 = g.abits[1], a2 = g.abits[2];
@@ -251,10 +256,10 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
           for (int k = 0; k < 4; k++) {
             const int row = rb | g.abits[k];
             const int qs = (mask & 4) ? qsel(g.abits[k]) : q;
-            const double2 x = reg_fetch_u<NQ>(v, qs, row * N + c);
+            const double2 xk = reg_fetch_u<NQ>(v, qs, row * N + c);
             // backward L = M^H: L[i][k] = conj(M[k][i]); forward L = M
             const double2 lk = fw ? M[i * 4 + k] : cconj(M[k * 4 + i]);
-            acc = k == 0 ? cmul(lk, x) : cfma(lk, x, acc);
+            acc = k == 0 ? cmul(lk, xk) : cfma(lk, xk, acc);
           }
           out[q] = acc;
         }
@@ -268,10 +273,10 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
           double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
           for (int k = 0; k < 4; k++) {
-            const double2 x = reg_fetch_u<NQ>(v, q, r * N + (cb | g.abits[k]));
+            const double2 xk = reg_fetch_u<NQ>(v, q, r * N + (cb | g.abits[k]));
             // backward R = M: R[k][j]; forward R = M^H: conj(M[j][k])
             const double2 rk = fw ? cconj(M[jj * 4 + k]) : M[k * 4 + jj];
-            acc = k == 0 ? cmul(x, rk) : cfma(x, rk, acc);
+            acc = k == 0 ? cmul(xk, rk) : cfma(xk, rk, acc);
           }
           out[q] = acc;
         }
@@ -281,13 +286,9 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
     };
     init();
     int it = 0;
-    if (A.max_iters > 0) prepare(0);
     for (;;) {
       if (A.max_iters > 0) {
-        for (int j = 0; j < steps; j++) {
-          sandwich(j);
-          if (j + 1 < steps) prepare(j + 1);
-        }
+        for (int j = 0; j < steps; j++) step(j);
         it++;
       }
       // cost + termination (readings R6-R10, R17), as k_lean
@@ -346,7 +347,6 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
       }
       if (vd != 0) break;
       if (it % A.reset_iters == 0) init();
-      prepare(0);
     }
     __syncwarp();
     for (int e = lane; e < gcount; e += 32) u_global[e] = gc[e];

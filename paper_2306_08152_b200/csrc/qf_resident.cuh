@@ -74,6 +74,7 @@ struct ResidentArgs {
   double2 *vstore;    // nullptr: cold Jacobi
   long long vstride;
   int *counter;       // work-stealing start counter (zeroed before launch)
+  const int *bad;     // non-null: input-check flags; nonzero = return at once
   const ResProb *probs;  // multi-problem launch: nprob problems, S = sum of starts
   int nprob;
   int polar_jacobi;   // 1: one-sided Jacobi instead of Newton-Schulz
@@ -882,6 +883,7 @@ __device__ __forceinline__ void res_grid_barrier(unsigned *gbar, unsigned nblock
 // pipe with 3 CTAs per SM in the sandwich, 54 % with one).
 template <int MAXD, bool MULTI, bool SMALL = false, bool WIDE = false>
 __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3) k_resident(const __grid_constant__ ResidentArgs A) {
+  if (A.bad != nullptr && *A.bad != 0) return;  // rejected input (host reports it)
   extern __shared__ __align__(128) unsigned char smraw[];
   // operand slots of SL complex each (WIDE: d <= 4 -> 16, else 64)
   constexpr int SL = WIDE ? 16 : 64;
