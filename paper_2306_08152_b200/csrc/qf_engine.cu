@@ -52,9 +52,9 @@ bool lean_ok(const qf_circuit_s &c, int maxm, bool warm) {
 
 // k_reg (the tensor in the warp's registers) where lean_ok holds and every
 // VARIABLE gate is one-qubit (closed-form polar factor), no R_z gates;
-// QF_REG=0 keeps k_lean (A/B, and the bitwise k_reg == k_lean tests)
+// QF_REG_RES=0 keeps k_lean (A/B, and the bitwise k_reg == k_lean tests)
 bool reg_ok(const qf_circuit_s &c) {
-  const char *e = getenv("QF_REG");
+  const char *e = getenv("QF_REG_RES");
   if (e && atoi(e) == 0) return false;
   for (int k = 0; k < c.p; k++) {
     if (c.kind[k] == QF_GATE_RZ) return false;

@@ -1,6 +1,6 @@
 """Smallest blocks (n <= 3): the register-resident kernel k_reg (tensor in the
 warp's registers, one-qubit VARIABLE gates, CONSTANT gates of <= 2 qubits)
-against the shared-memory kernel k_lean it replaces (QF_REG=0) -- bitwise
+against the shared-memory kernel k_lean it replaces (QF_REG_RES=0) -- bitwise
 equal summaries, gates and per-sweep records, since every output is formed
 with k_lean's operand and summation order -- and against the oracle within the
 north_star tolerance.  Templates cover every gate position at n = 1, 2, 3
@@ -46,9 +46,9 @@ def _template(n, p, seed):
 
 def _both(c, V, init, monkeypatch, **kw):
     a = qf.qf_instantiate(c, V, init, **kw)
-    monkeypatch.setenv("QF_REG", "0")
+    monkeypatch.setenv("QF_REG_RES", "0")
     b = qf.qf_instantiate(c, V, init, **kw)
-    monkeypatch.delenv("QF_REG")
+    monkeypatch.delenv("QF_REG_RES")
     assert a.stats["resident_kernel"] == 3 and b.stats["resident_kernel"] == 2
     return a, b
 

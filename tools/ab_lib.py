@@ -3,7 +3,8 @@
 SPEC = path/to/lib.so[@VAR=value[,VAR=value]] (environment for that arm).
 C4 (or `config`), 3 sweeps (or --sweeps K), resident engine (AB_ENGINE=stream for the
 streaming one); alternates the arms to cancel drift and prints each run's
-wall time of the whole call (ms, best of the last two of three)."""
+wall time of the whole call (ms, best of the last two of three), the
+start-sweeps it ran and the time per start-sweep."""
 import ctypes
 import os
 import subprocess
@@ -45,10 +46,10 @@ ms = []
 for _ in range(3):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=MI, engine=eng, want_result=False)
+    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=MI, engine=eng)
     torch.cuda.synchronize()
     ms.append(1e3 * (time.perf_counter() - t0))
-print(min(ms[1:]))
+print(r.stats["start_sweeps"], min(ms[1:]))
 ''' % ROOT
 res = {l: [] for l in libs}
 for _ in range(reps):
@@ -60,6 +61,10 @@ for _ in range(reps):
             env[k] = v
         out = subprocess.run([sys.executable, "-c", code, path, cfg, str(sweeps)], capture_output=True, text=True,
                              env=env)
-        res[l].append(float(out.stdout.strip().split()[-1]))
+        f = out.stdout.strip().split()
+        res[l].append((float(f[-1]), int(f[-2])))
 for l in libs:
-    print(l, " ".join(f"{x:.2f}" for x in res[l]), "min", f"{min(res[l]):.2f}")
+    t = [x for x, _ in res[l]]
+    ss = res[l][0][1]
+    print(l, " ".join(f"{x:.2f}" for x in t), "min", f"{min(t):.2f}", "start-sweeps", ss,
+          f"us/start-sweep {1e3 * min(t) / ss:.4f}")
