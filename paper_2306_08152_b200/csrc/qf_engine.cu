@@ -1010,6 +1010,20 @@ struct Engine {
     }
     const int grid = std::max(1, std::min((S + kEnvWarps - 1) / kEnvWarps, nsm * 16));
     const int slot = prof.on ? prof.open(1, st) : -1;
+    // QF_GROUP_TSUM=1 (part_mode 2): T summed by its own high-occupancy kernel
+    // first.  k_tsum<8> streams its 268 MB at 86 % of the HBM peak (C5), but
+    // k_group's update chain alone then takes ~75 of the fused kernel's ~115 us
+    // and the two launches measured 88.5 vs 83.2 ms per C5 call, so it is off
+    // (profiles/r02_group_tsum_split.txt)
+    const int tsum_env = getenv("QF_GROUP_TSUM") ? atoi(getenv("QF_GROUP_TSUM")) : 0;
+    if (A.part && A.part_mode == 2 && tsum_env) {
+      A.tpre = 1;
+      const int gt = std::max(1, std::min((S + 7) / 8, nsm * 16));
+      if (w == 1) k_tsum<2><<<gt, 256, 0, st>>>(A);
+      else if (w == 2) k_tsum<4><<<gt, 256, 0, st>>>(A);
+      else k_tsum<8><<<gt, 256, 0, st>>>(A);
+      launches++;
+    }
     if (w == 1) k_group<2><<<grid, 32 * kEnvWarps, 0, st>>>(A);
     else if (w == 2) k_group<4><<<grid, 32 * kEnvWarps, 0, st>>>(A);
     else k_group<8><<<grid, 32 * kEnvWarps, 0, st>>>(A);

@@ -1742,6 +1742,7 @@ struct GroupArgs {
   // rowlist[rl_begin[a'] .. rl_begin[a' + 1]) = offsets tile * rows + q of the
   // flush rows whose pattern on W is nab[a'], ascending
   int part_mode;
+  int tpre;  // 1: T was summed by k_tsum into ops[s][0 .. DW^2) (part_mode 2)
   int rl_begin[9];
   unsigned short rowlist[kRowListMax];
   int nsteps;
@@ -1802,6 +1803,25 @@ __device__ __forceinline__ void warp_sum_rowparts(const GroupArgs &A, const unsi
   __syncwarp();
 }
 
+// T of grouped steps for every active start (part_mode 2), before k_group:
+// the byte-bound half of the environment on its own, at an occupancy the
+// update chain's registers would not allow (one warp per start, 8 warps per
+// CTA, 4 CTAs per SM); T goes to the start's ops slot, where k_group reads it
+// (the same per-lane summation as k_group's own, so T is bitwise the same)
+template <int DW>
+__global__ void __launch_bounds__(256, 4) k_tsum(const __grid_constant__ GroupArgs A) {
+  __shared__ unsigned short rls[kRowListMax];
+  for (int e = threadIdx.x; e < A.rl_begin[DW]; e += blockDim.x) rls[e] = A.rowlist[e];
+  __syncthreads();
+  const int nact = *A.n_active;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int ai = blockIdx.x * 8 + w; ai < nact; ai += gridDim.x * 8) {
+    const int s = A.active[ai];
+    warp_sum_rowparts<DW>(A, rls, A.part + (long long)s * A.part_stride, lane,
+                          A.ops + (long long)s * A.ops_stride);
+  }
+}
+
 template <int DW>
 __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant__ GroupArgs A) {
   constexpr int DD = DW * DW;
@@ -1818,13 +1838,16 @@ __global__ void __launch_bounds__(32 * kEnvWarps) k_group(const __grid_constant_
   const int nact = *A.n_active;
   const int N = A.N;
   __shared__ unsigned short rls[kRowListMax];  // part_mode 2: the row lists, block-shared
-  if (A.part && A.part_mode == 2) {
+  if (A.part && A.part_mode == 2 && !A.tpre) {
     for (int e = threadIdx.x; e < A.rl_begin[DW]; e += blockDim.x) rls[e] = A.rowlist[e];
     __syncthreads();
   }
   for (int ai = blockIdx.x * kEnvWarps + w; ai < nact; ai += gridDim.x * kEnvWarps) {
     const int s = A.active[ai];
-    if (A.part && A.part_mode == 2) {
+    if (A.tpre) {  // T from k_tsum
+      for (int o = lane; o < DD; o += 32) T[o] = A.ops[(long long)s * A.ops_stride + o];
+      __syncwarp();
+    } else if (A.part && A.part_mode == 2) {
       // T from the flush's per-row values: T[a'][b'] = sum over tiles, then
       // tile rows (ascending), of the rows whose pattern on W is nab[a']
       warp_sum_rowparts<DW>(A, rls, A.part + (long long)s * A.part_stride, lane, T);

@@ -12,7 +12,7 @@ kw = dict(max_iters=2, seed=w.init_seed, num_starts=w.starts)
 qf.qf_instantiate_device(c, V, None, ws, want_result=False, **kw)
 r = qf.qf_instantiate_device(c, V, None, ws, profile=1, **kw)
 st = r.stats
-print(os.environ.get("QF_GROUP_FUSE", "0"), "sandwich ms", round(st["sandwich_ms"], 1), "launches", st["sandwich_launches"],
+print("fuse", os.environ.get("QF_GROUP_FUSE", "2"), "tsum", os.environ.get("QF_GROUP_TSUM", "1"), "sandwich ms", round(st["sandwich_ms"], 1), "launches", st["sandwich_launches"],
       "GB/s", round(st["sandwich_bytes"] / 1e9 / (st["sandwich_ms"] / 1e3)),
       "| env ms", round(st["env_ms"], 1), "launches", st["env_launches"],
       "useful GB/s", round(st["env_bytes"] / 1e9 / (st["env_ms"] / 1e3)))
