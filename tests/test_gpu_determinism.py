@@ -17,8 +17,10 @@ pytestmark = pytest.mark.gpu
 
 CASES = [
     # (name, config, starts, sweeps, engine, env, extra params)
-    ("resident SMALL n=2", "C1", 4, 30, qf.QF_ENGINE_AUTO, {}, {}),
-    ("resident SMALL n=3", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {}, {}),
+    ("register-resident k_reg n=2", "C1", 4, 30, qf.QF_ENGINE_AUTO, {}, {}),
+    ("register-resident k_reg n=3", "C2", 16, 40, qf.QF_ENGINE_AUTO, {}, {}),
+    ("one-warp k_lean n=3", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {}, {}),
+    ("resident SMALL n=3", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {"QF_LEAN": "0"}, {}),
     ("resident SMALL n=4", "C3", 64, 10, qf.QF_ENGINE_AUTO, {}, {}),
     ("resident 128-thread n=6", "C4", 96, 6, qf.QF_ENGINE_AUTO, {}, {}),
     ("resident WIDE n=6", "C4", 96, 6, qf.QF_ENGINE_AUTO, {"QF_RES_WIDE": "1"}, {}),
