@@ -644,6 +644,20 @@ __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U,
       const unsigned cq = !(ax <= 0.55 && ay <= 0.55) ? 2u : (!(ax <= 1e-5 && ay <= 1e-5) ? 1u : 0u);
       code = cq > code ? cq : code;
     }
+    __syncwarp();
+    // Y^2 first: it does not depend on the tests, so it overlaps the reduction
+    double2 zq[OPL];
+#pragma unroll
+    for (int q = 0; q < OPL; q++) {
+      const int r = oo[q] / D, c = oo[q] % D;
+      double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0;
+#pragma unroll
+      for (int k = 0; k < D; k += 2) {
+        acc0 = cfma(Ym[r * D + k], Ym[k * D + c], acc0);
+        acc1 = cfma(Ym[r * D + k + 1], Ym[(k + 1) * D + c], acc1);
+      }
+      zq[q] = cadd(acc0, acc1);
+    }
     code = __reduce_max_sync(0xffffffffu, code);
     // a singular value still below ~0.45 after 8 steep + 8 cubic steps was
     // below ~2e-7 sigma_max at the start (growth >= 3.44^8 1.875^8): A is
@@ -654,17 +668,10 @@ __device__ bool warp_polar_ns(double2 *Xm, double2 *Ym, double2 *Wm, double2 *U,
     if (fast) fast = it < 8 && code == 2;
     const double ca = fast ? 3.4445 : 1.875, cb = fast ? -4.7750 : -1.25,
                  cc = fast ? 2.0315 : 0.375;
-    __syncwarp();
 #pragma unroll
     for (int q = 0; q < OPL; q++) {  // W = ca I + cb Y + cc Y^2
       const int r = oo[q] / D, c = oo[q] % D;
-      double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0;
-#pragma unroll
-      for (int k = 0; k < D; k += 2) {
-        acc0 = cfma(Ym[r * D + k], Ym[k * D + c], acc0);
-        acc1 = cfma(Ym[r * D + k + 1], Ym[(k + 1) * D + c], acc1);
-      }
-      const double2 z = cadd(acc0, acc1);
+      const double2 z = zq[q];
       const double2 w = make_double2(fma(cc, z.x, fma(cb, y[q].x, r == c ? ca : 0.0)),
                                      fma(cc, z.y, cb * y[q].y));
       if (wr[q]) Wm[oo[q]] = w;
@@ -761,6 +768,12 @@ __device__ bool warp_polar_ns_mma4(double2 *Am, double2 *U, int lane) {
       y0 *= s2;
       y1 *= s2;
     }
+    // Y^2 does not depend on the tests below: issued first, so its shuffles
+    // and MMAs overlap the warp reduction
+    const double yf0 = mma_rowfrag(y0, y1, 0, lane), yf1 = mma_rowfrag(y0, y1, 1, lane);
+    double z0 = 0.0, z1 = 0.0;  // Y^2
+    ptx::dmma(z0, z1, yf0, yf0);
+    ptx::dmma(z0, z1, yf1, yf1);
     // 2 = some |Y - I| entry > 0.55 (or NaN), 1 = some > 1e-5, 0 = converged
     unsigned code = 0;
 #pragma unroll
@@ -775,10 +788,6 @@ __device__ bool warp_polar_ns_mma4(double2 *Am, double2 *U, int lane) {
     if (fast) fast = it < 8 && code == 2;
     const double ca = fast ? 3.4445 : 1.875, cb = fast ? -4.7750 : -1.25,
                  cc = fast ? 2.0315 : 0.375;
-    const double yf0 = mma_rowfrag(y0, y1, 0, lane), yf1 = mma_rowfrag(y0, y1, 1, lane);
-    double z0 = 0.0, z1 = 0.0;  // Y^2
-    ptx::dmma(z0, z1, yf0, yf0);
-    ptx::dmma(z0, z1, yf1, yf1);
     const double w0 = fma(cc, z0, fma(cb, y0, m == 2 * q ? ca : 0.0));
     const double w1 = fma(cc, z1, fma(cb, y1, m == 2 * q + 1 ? ca : 0.0));
     const double wf0 = mma_rowfrag(w0, w1, 0, lane), wf1 = mma_rowfrag(w0, w1, 1, lane);

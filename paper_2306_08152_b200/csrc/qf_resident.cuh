@@ -158,6 +158,11 @@ __device__ __forceinline__ int sidxw(int i, int j, int N) {
 __device__ __forceinline__ int rspread(const GateDesc &g, int n, int r) {
   return insert_zeros(r, g.mask);
 }
+// the same for a 2-qubit gate with basis bits p0 < p1, branch-free
+__device__ __forceinline__ int rspread2(int r, int p0, int p1) {
+  r = ((r >> p0) << (p0 + 1)) | (r & ((1 << p0) - 1));
+  return ((r >> p1) << (p1 + 1)) | (r & ((1 << p1) - 1));
+}
 
 // ct <- E(L) ct E(R) in place for D <= 4, one D x D block (row-rest r,
 // column-rest c) per item held in registers: one shared-memory read and write
@@ -168,9 +173,11 @@ __device__ void res_sandwich_blocks(double2 *ct, const GateDesc &g, int n, int N
                                     const double2 *Ls, const double2 *Rs, int t0, int nt) {
   constexpr int LD = D == 2 ? 1 : (D == 4 ? 2 : 3);
   const int lnr = n - LD, NR = 1 << lnr;  // N / D rests (no runtime division)
+  const int p0 = __ffs(g.mask) - 1, p1 = 31 - __clz(g.mask);
   for (int it = t0; it < NR * NR; it += nt) {
     const int r = it >> lnr, c = it & (NR - 1);
-    const int rb = rspread(g, n, r), cb = rspread(g, n, c);
+    const int rb = D == 4 ? rspread2(r, p0, p1) : rspread(g, n, r);
+    const int cb = D == 4 ? rspread2(c, p0, p1) : rspread(g, n, c);
     double2 x[D][D];
 #pragma unroll
     for (int a = 0; a < D; a++)
@@ -391,8 +398,9 @@ __device__ void res_gather_d(const ResidentArgs &A, const ResView &V, const doub
     double2 acc = make_double2(0.0, 0.0);
     if (o < DD) {
       const int a = o / D, b = o % D;
+      const int p0 = __ffs(g.mask) - 1, p1 = 31 - __clz(g.mask);
       for (int r = k; r < R; r += tpo) {
-        const int sp = rspread(g, V.n, r);
+        const int sp = D == 4 ? rspread2(r, p0, p1) : rspread(g, V.n, r);
         const double2 v = ct[sidxw<WS>(sp | g.abits[a], sp | g.abits[b], N)];
         acc.x += v.x;
         acc.y += v.y;
@@ -599,7 +607,7 @@ template <int MAXD, bool SMALL = false, bool WIDE = false>
 __device__ __forceinline__ void res_apply(double2 *ct, const GateDesc &g, const ResView &V,
                                           const double2 *Lb, const double2 *Rb, const int *tab,
                                           int t0, int nt, int ilp = 4) {
-  const int nb = V.N / g.d;
+  const int nb = V.N >> (31 - __clz(g.d));  // V.N / g.d (powers of two)
   const bool blocks = !SMALL && nb * nb >= nt;
   if (g.d == 2) {
     // 2 x 2 register blocks (8 registers) also in SMALL launches: one
