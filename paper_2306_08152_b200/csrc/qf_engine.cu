@@ -1241,6 +1241,32 @@ std::vector<GateDesc> make_gdesc(const qf_circuit_s &c, const std::vector<int> *
     g.goff = g.kind != 1 ? c.var_off[k] / 2 : c.const_off[k] / 2;
     g.mask = b.abits[b.d - 1];
     g.voff = voff && g.kind != 1 ? (*voff)[k] : 0;
+    if (g.kind == 1 && g.d == 4) {
+      // a CONSTANT 4 x 4 0/1 permutation (CNOT, SWAP, ...): the step is an
+      // exact relabelling of ct; voff carries kGatePerm |
+      // pi^-1 << 8 | pi (2 bits per local index, M[i][pi(i)] = 1)
+      const double *M = c.const_mats.data() + c.const_off[k];
+      int pi = 0, pinv = 0;
+      bool perm = true;
+      for (int i = 0; i < 4 && perm; i++) {
+        int ones = 0, at = -1;
+        for (int j = 0; j < 4; j++) {
+          const double re = M[2 * (i * 4 + j)], im = M[2 * (i * 4 + j) + 1];
+          if (re == 1.0 && im == 0.0) {
+            ones++;
+            at = j;
+          } else if (!(re == 0.0 && im == 0.0)) {
+            perm = false;
+          }
+        }
+        if (ones != 1) perm = false;
+        if (perm) {
+          pi |= at << (2 * i);
+          pinv |= i << (2 * at);
+        }
+      }
+      if (perm) g.voff = kGatePerm | (pinv << 8) | pi;
+    }
     for (int a = 0; a < 8; a++) g.abits[a] = a < b.d ? b.abits[a] : 0;
     for (int q = 0; q < kMaxQubits; q++) g.rest_pos[q] = q < c.n - b.m ? b.rest_pos[q] : 0;
     g.pbit = pick_pair_bit(b);

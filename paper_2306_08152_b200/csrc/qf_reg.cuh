@@ -243,6 +243,24 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
 #pragma unroll
         for (int q = 0; q < EPL; q++) v[q] = out[q];
         __syncwarp();  // u_new visible to the next step's u_old load
+      } else if (g.voff & kGatePerm) {
+        // CONSTANT 0/1 permutation M[i][pi(i)] = 1: backward M^H ct M takes
+        // element (pi^-1(i), pi^-1(j)) of the gate's block, forward M ct M^H
+        // element (pi(i), pi(j)) -- the dense passes' exact result (products
+        // with 1 and sums with 0), one fetch per element
+        const int sig = fw ? (g.voff & 0xff) : ((g.voff >> 8) & 0xff);
+        const int a1 = g.abits[1], a2 = g.abits[2];
+#pragma unroll
+        for (int q = 0; q < EPL; q++) {
+          const int r = eo[q] >> NQ, c = eo[q] & (N - 1);
+          const int i = (((r & a2) != 0) << 1) | ((r & a1) != 0);
+          const int jj = (((c & a2) != 0) << 1) | ((c & a1) != 0);
+          const int si = (sig >> (2 * i)) & 3, sj = (sig >> (2 * jj)) & 3;
+          const int row = (r & ~mask) | g.abits[si], col = (c & ~mask) | g.abits[sj];
+          out[q] = reg_fetch_any<NQ>(v, row * N + col);
+        }
+#pragma unroll
+        for (int q = 0; q < EPL; q++) v[q] = out[q];
       } else {  // CONSTANT 4 x 4: left pass, then right pass (k_lean pass4)
         const double2 *M = cm + g.goff;
         const int a1 = g.abits[1], a2 = g.abits[2];

@@ -23,6 +23,9 @@ __device__ unsigned long long qf_t_gather, qf_t_form, qf_t_polar, qf_n_upd;
 __device__ unsigned long long qf_t_ovl[4];  // WIDE phase A on warp 0: env, staged, prepare; steps
 #endif
 
+// GateDesc.voff of a CONSTANT 4 x 4 permutation gate (k_reg relabels ct)
+constexpr int kGatePerm = 1 << 16;
+
 struct GateDesc {
   int m, d, kind, goff;   // kind 0 VARIABLE, 1 CONSTANT, 2 RZ; goff: complex offset in the
                           // packed gates (VARIABLE, RZ) or in cmats (CONSTANT)
