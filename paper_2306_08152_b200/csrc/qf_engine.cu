@@ -50,15 +50,15 @@ bool lean_ok(const qf_circuit_s &c, int maxm, bool warm) {
          (long long)c.var_doubles / 2 + (long long)c.const_mats.size() / 2 <= 4096;
 }
 
-// k_reg (the tensor in the warp's registers) where lean_ok holds and every
-// VARIABLE gate is one-qubit (closed-form polar factor), no R_z gates;
+// k_reg (the tensor in the warp's registers) where lean_ok holds and there
+// are no R_z gates;
 // QF_REG_RES=0 keeps k_lean (A/B, and the bitwise k_reg == k_lean tests)
 bool reg_ok(const qf_circuit_s &c) {
   const char *e = getenv("QF_REG_RES");
   if (e && atoi(e) == 0) return false;
   for (int k = 0; k < c.p; k++) {
     if (c.kind[k] == QF_GATE_RZ) return false;
-    if (c.kind[k] == QF_GATE_VARIABLE && c.arity[k] != 1) return false;
+    if (c.kind[k] == QF_GATE_VARIABLE && c.arity[k] > 2) return false;
   }
   return true;
 }
@@ -1532,7 +1532,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       // n <= 3, gates <= 2 qubits: one warp per start (k_reg: tensor in
       // registers, one-qubit VARIABLE gates; else k_lean: in shared memory)
       const bool rg = reg_ok(c);
-      const size_t lsm = ((size_t)(rg ? 0 : kLeanFixed) + A.gstride + A.ncm) * 16;
+      const size_t lsm = ((size_t)(rg ? kRegFixed : kLeanFixed) + A.gstride + A.ncm) * 16;
       const bool bt = p.beta != 0.0;
       auto lk = rg ? (c.n == 1 ? (bt ? k_reg<1, true> : k_reg<1, false>)
                       : c.n == 2 ? (bt ? k_reg<2, true> : k_reg<2, false>)

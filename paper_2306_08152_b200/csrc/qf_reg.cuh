@@ -52,13 +52,17 @@ __device__ __forceinline__ double2 reg_fetch_u(const double2 (&v)[RegShape<NQ>::
   }
 }
 
+constexpr int kRegFixed = 6 * 16;  // L, R, u_old, P, A, V of a 4 x 4 VARIABLE update
+
 template <int NQ, bool BETA>
 __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs A) {
   if (A.bad != nullptr && *A.bad != 0) return;  // rejected input (host reports it)
   using RS = RegShape<NQ>;
   constexpr int N = RS::N, EPL = RS::EPL;
   extern __shared__ __align__(16) double2 rsm[];
-  double2 *gc = rsm;  // the start's gates, then the CONSTANT matrices
+  // 4 x 4 VARIABLE updates: operands L, R and the polar factor's buffers
+  double2 *Lb = rsm, *Rb = Lb + 16, *Uo = Rb + 16, *Pm = Uo + 16, *Am = Pm + 16, *Vm = Am + 16;
+  double2 *gc = rsm + kRegFixed;  // the start's gates, then the CONSTANT matrices
   const int lane = threadIdx.x, p = A.p, steps = 2 * p;
   const int gcount = (int)A.gstride;
   for (int e = lane; e < A.ncm; e += 32) gc[gcount + e] = A.cmats[e];
@@ -261,9 +265,64 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
         }
 #pragma unroll
         for (int q = 0; q < EPL; q++) v[q] = out[q];
-      } else {  // CONSTANT 4 x 4: left pass, then right pass (k_lean pass4)
+      } else {  // 4 x 4: left pass, then right pass (k_lean pass4)
         const double2 *M = cm + g.goff;
         const int a1 = g.abits[1], a2 = g.abits[2];
+        const bool var4 = g.kind != 1;
+        if (var4) {
+          // VARIABLE (as k_lean's prepare): P = PT(ct) on lanes 0..15 (rests
+          // ascending), A = E^dagger, warp_polar, then L / R in shared memory
+          const int p0 = __ffs(mask) - 1, p1 = 31 - __clz(mask);
+          double2 *u = gc + g.goff;
+          {  // every lane runs the shuffles (lanes 16..31 duplicate 0..15)
+            const int l16 = lane & 15;
+            const int ra = g.abits[l16 >> 2], rc = g.abits[l16 & 3];
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 0; r < N / 4; r++) {
+              const int rb = insert2(r, p0, p1);
+              const double2 xe = reg_fetch_any<NQ>(v, (rb | ra) * N + (rb | rc));
+              acc.x += xe.x;
+              acc.y += xe.y;
+            }
+            if (lane < 16) {
+              Uo[lane] = u[lane];
+              Pm[lane] = acc;
+            }
+          }
+          __syncwarp();
+          if (lane < 16) {
+            const int r = lane >> 2, c = lane & 3;
+            double2 acc = make_double2(0.0, 0.0);
+            if (!fw) {
+              for (int k = 0; k < 4; k++) acc = cfma_cj(Pm[k * 4 + r], Uo[k * 4 + c], acc);
+            } else {
+              for (int k = 0; k < 4; k++) {
+                const double2 x = Uo[r * 4 + k], pv = Pm[c * 4 + k];
+                acc.x = fma(x.x, pv.x, acc.x);
+                acc.x = fma(x.y, pv.y, acc.x);
+                acc.y = fma(x.y, pv.x, acc.y);
+                acc.y = fma(-x.x, pv.y, acc.y);
+              }
+            }
+            if constexpr (BETA) {
+              acc = cscale(acc, 1.0 - A.beta);
+              acc.x = fma(A.beta, Uo[lane].x, acc.x);
+              acc.y = fma(A.beta, Uo[lane].y, acc.y);
+            }
+            Am[lane] = acc;
+          }
+          __syncwarp();
+          warp_polar<4>(Am, Vm, Pm, lane, nullptr, A.polar_jacobi != 0, A.polar_mma != 0);
+          if (lane < 16) {
+            u[lane] = Pm[lane];  // u_new
+            const int i = lane >> 2, k = lane & 3;
+            const double2 od = cconj(Uo[k * 4 + i]);
+            Lb[lane] = fw ? Pm[lane] : od;
+            Rb[lane] = fw ? od : Pm[lane];
+          }
+          __syncwarp();
+        }
 #pragma unroll
         for (int q = 0; q < EPL; q++) {
           const int r = eo[q] >> NQ, c = eo[q] & (N - 1);
@@ -276,7 +335,7 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
             const int qs = (mask & 4) ? qsel(g.abits[k]) : q;
             const double2 xk = reg_fetch_u<NQ>(v, qs, row * N + c);
             // backward L = M^H: L[i][k] = conj(M[k][i]); forward L = M
-            const double2 lk = fw ? M[i * 4 + k] : cconj(M[k * 4 + i]);
+            const double2 lk = var4 ? Lb[i * 4 + k] : (fw ? M[i * 4 + k] : cconj(M[k * 4 + i]));
             acc = k == 0 ? cmul(lk, xk) : cfma(lk, xk, acc);
           }
           out[q] = acc;
@@ -293,7 +352,7 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
           for (int k = 0; k < 4; k++) {
             const double2 xk = reg_fetch_u<NQ>(v, q, r * N + (cb | g.abits[k]));
             // backward R = M: R[k][j]; forward R = M^H: conj(M[j][k])
-            const double2 rk = fw ? cconj(M[jj * 4 + k]) : M[k * 4 + jj];
+            const double2 rk = var4 ? Rb[k * 4 + jj] : (fw ? cconj(M[jj * 4 + k]) : M[k * 4 + jj]);
             acc = k == 0 ? cmul(xk, rk) : cfma(xk, rk, acc);
           }
           out[q] = acc;

@@ -1,5 +1,6 @@
 """Smallest blocks (n <= 3): the register-resident kernel k_reg (tensor in the
-warp's registers, one-qubit VARIABLE gates, CONSTANT gates of <= 2 qubits)
+warp's registers; VARIABLE and CONSTANT gates of <= 2 qubits, CONSTANT 0/1
+permutations applied as relabellings)
 against the shared-memory kernel k_lean it replaces (QF_REG_RES=0) -- bitwise
 equal summaries, gates and per-sweep records, since every output is formed
 with k_lean's operand and summation order -- and against the oracle within the
@@ -19,14 +20,20 @@ pytestmark = pytest.mark.gpu
 CNOT = np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]], dtype=complex)
 
 
-def _template(n, p, seed):
+def _template(n, p, seed, var2=0.0):
     """One-qubit VARIABLE gates on random qubits, CONSTANT CNOT / Haar 4 x 4
-    on random ordered pairs (any order, any distance), CONSTANT Haar 2 x 2."""
+    on random ordered pairs (any order, any distance), CONSTANT Haar 2 x 2;
+    with probability var2 a 2-qubit VARIABLE gate on a random ordered pair."""
     rng = np.random.default_rng(seed)
     locs, kinds, cm = [], [], []
     for k in range(p):
         u = rng.random()
-        if n >= 2 and u < 0.35:
+        if n >= 2 and rng.random() < var2:
+            q = rng.choice(n, 2, replace=False)
+            locs.append((int(q[0]), int(q[1])))
+            kinds.append(qfgen.VARIABLE)
+            cm.append(None)
+        elif n >= 2 and u < 0.35:
             q = rng.choice(n, 2, replace=False)
             locs.append((int(q[0]), int(q[1])))
             kinds.append(qfgen.CONSTANT)
@@ -61,7 +68,7 @@ def _same(a, b):
         assert np.array_equal(a.gates_hist, b.gates_hist, equal_nan=True)
 
 
-@pytest.mark.parametrize("name,iters", [("C1", None), ("C2", 300)])
+@pytest.mark.parametrize("name,iters", [("C1", None), ("C2", 300), ("C2+", None)])
 def test_reg_bitwise_lean_configs(name, iters, monkeypatch):
     w = qfgen.workload(name)
     c = qf.Circuit.from_workload(w)
@@ -72,16 +79,19 @@ def test_reg_bitwise_lean_configs(name, iters, monkeypatch):
     _same(a, b)
 
 
-@pytest.mark.parametrize("n,p,seed,params", [
-    (1, 3, 1, {}),
-    (2, 9, 2, {}),
-    (2, 14, 3, {"beta": 0.1, "reset_iters": 7}),
-    (3, 12, 4, {}),
-    (3, 30, 5, {"reset_iters": 5}),
-    (3, 20, 6, {"beta": 0.05}),
+@pytest.mark.parametrize("n,p,seed,var2,params", [
+    (1, 3, 1, 0.0, {}),
+    (2, 9, 2, 0.0, {}),
+    (2, 14, 3, 0.0, {"beta": 0.1, "reset_iters": 7}),
+    (3, 12, 4, 0.0, {}),
+    (3, 30, 5, 0.0, {"reset_iters": 5}),
+    (3, 20, 6, 0.0, {"beta": 0.05}),
+    (2, 10, 7, 0.4, {}),
+    (3, 16, 8, 0.4, {"beta": 0.05, "reset_iters": 6}),
+    (3, 24, 9, 0.3, {}),
 ])
-def test_reg_bitwise_lean_random(n, p, seed, params, monkeypatch):
-    locs, kinds, cm = _template(n, p, seed)
+def test_reg_bitwise_lean_random(n, p, seed, var2, params, monkeypatch):
+    locs, kinds, cm = _template(n, p, seed, var2)
     c = qf.Circuit(n, locs, kinds, cm)
     V = qfgen.haar(qfgen.stream_key(seed, qfgen.PURPOSE_TARGET, 0, 0), 2 ** n)[0]
     init = qfgen.initial_gates(n, locs, kinds, 4000 + seed, 0, 37)
@@ -90,11 +100,12 @@ def test_reg_bitwise_lean_random(n, p, seed, params, monkeypatch):
     _same(a, b)
 
 
-@pytest.mark.parametrize("n,p,seed", [(2, 9, 12), (3, 16, 13), (3, 24, 14)])
-def test_reg_parity_oracle(n, p, seed):
+@pytest.mark.parametrize("n,p,seed,var2", [(2, 9, 12, 0.0), (3, 16, 13, 0.0), (3, 24, 14, 0.0),
+                                            (3, 14, 15, 0.4)])
+def test_reg_parity_oracle(n, p, seed, var2):
     """k_reg against the oracle: 37 starts, 10 recorded sweeps, to verdict
     within 300 sweeps (north_star tolerance, R21 readings as in test_gpu_parity)."""
-    locs, kinds, cm = _template(n, p, seed)
+    locs, kinds, cm = _template(n, p, seed, var2)
     V = qfgen.haar(qfgen.stream_key(seed, qfgen.PURPOSE_TARGET, 0, 0), 2 ** n)[0]
     init = qfgen.initial_gates(n, locs, kinds, 4000 + seed, 0, 37)
     gpu, orc, idx = _run_pair(n, locs, kinds, cm, V, init, R=10, max_iters=300)
