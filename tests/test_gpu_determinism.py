@@ -19,7 +19,8 @@ CASES = [
     # (name, config, starts, sweeps, engine, env, extra params)
     ("register-resident k_reg n=2", "C1", 4, 30, qf.QF_ENGINE_AUTO, {}, {}),
     ("register-resident k_reg n=3", "C2", 16, 40, qf.QF_ENGINE_AUTO, {}, {}),
-    ("one-warp k_lean n=3", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {}, {}),
+    ("register-resident k_reg n=3, 2-qubit VARIABLE", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {}, {}),
+    ("one-warp k_lean n=3", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {"QF_REG_RES": "0"}, {}),
     ("resident SMALL n=3", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {"QF_LEAN": "0"}, {}),
     ("resident SMALL n=4", "C3", 64, 10, qf.QF_ENGINE_AUTO, {}, {}),
     ("resident 128-thread n=6", "C4", 96, 6, qf.QF_ENGINE_AUTO, {}, {}),

@@ -3,8 +3,8 @@ synccheck, memcheck; one tool per gpurun call, B200_PROFILING.md):
 
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py [case ...]
 
-resident engine: C1 / C2 (register-resident k_reg), C2+ (k_lean and the SMALL
-k_resident variant), C3 (SMALL variant, n <= 4), C4 (128-thread
+resident engine: C1 / C2 / C2+ (register-resident k_reg), C2+ also on k_lean and
+the SMALL k_resident variant, C3 (SMALL variant, n <= 4), C4 (128-thread
 kernel), C4 WIDE (256-thread MMA variant, overlapped steps), C3+ under the
 paper's batch policy (cooperative launch, grid barrier per sweep), many
 (heterogeneous problems in one launch); streaming engine: C4 (register
@@ -44,7 +44,8 @@ def run(name, S, iters, engine=qf.QF_ENGINE_AUTO, env=None, **kw):
 CASES = {
     "res_C1": lambda: run("C1", 4, 20),                        # k_reg<2>
     "res_C2": lambda: run("C2", 8, 20),                        # k_reg<3>
-    "res_C2p": lambda: run("C2+", 8, 10),                      # k_lean<3>
+    "res_C2p": lambda: run("C2+", 8, 10),                      # k_reg<3>, 2-qubit VARIABLE
+    "res_C2p_lean": lambda: run("C2+", 8, 10, env={"QF_REG_RES": "0"}),  # k_lean<3>
     "res_C2p_small": lambda: run("C2+", 8, 10, env={"QF_LEAN": "0"}),
     "res_C3": lambda: run("C3", 16, 3),
     "res_C4": lambda: run("C4", 6, 2),
