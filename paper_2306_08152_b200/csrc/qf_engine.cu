@@ -279,14 +279,6 @@ __global__ void k_check_gates(const double *G, long long S, int nvar, const int2
   }
 }
 
-__global__ void k_iota(int *active, int *n_active, int S, int *rec_slot) {
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
-    active[s] = s;
-    rec_slot[s] = -1;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *n_active = S;
-}
-
 __global__ void k_set_slots(int *rec_slot, const int *starts, int count) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) rec_slot[starts[i]] = i;
@@ -300,17 +292,6 @@ __global__ void k_ct_from_vdag(double2 *ct, long long NN, const double2 *Vd, con
        e += (long long)gridDim.x * blockDim.x) {
     const long long ai = e / NN, k = e - ai * NN;
     ct[(long long)active[ai] * NN + k] = Vd[k];
-  }
-}
-
-__global__ void k_summaries(const double *delta, const int *iters, const int *verdict, int S,
-                            qf_summary *out) {
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x) {
-    qf_summary q;
-    q.delta = delta[s];
-    q.iters = iters[s];
-    q.verdict = verdict[s];
-    out[s] = q;
   }
 }
 
@@ -333,6 +314,89 @@ __global__ void __launch_bounds__(1024) k_select_best(const qf_summary *q, long 
     if (bi < 0 || better(d, i, bd, bi)) {
       bd = d;
       bi = i;
+    }
+  }
+  sd[threadIdx.x] = bd;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      const double d2 = sd[threadIdx.x + off];
+      const long long i2 = si[threadIdx.x + off];
+      if (i2 >= 0 && (si[threadIdx.x] < 0 || better(d2, i2, sd[threadIdx.x], si[threadIdx.x]))) {
+        sd[threadIdx.x] = d2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *best = si[0];
+}
+
+// a1 in one launch (single-problem calls): V^dagger and the target check per
+// (i, j), the initial gates' checks per (start, gate), their copy into the
+// workspace, the active list / record slots, and the resident start counter
+__global__ void k_stage(const double2 *V, double2 *Vd, int N, double tol, int *bad,
+                        const double *G_in, double *G, long long S, int nvar, const int2 *tab,
+                        int var_doubles, int *active, int *n_active, int *rec_slot, int *counter) {
+  const long long NN = (long long)N * N, str = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long e = t0; e < NN; e += str) {
+    const int i = (int)(e / N), j = (int)(e % N);
+    const double2 v = V[(long long)j * N + i];
+    Vd[e] = make_double2(v.x, -v.y);
+    double2 acc = make_double2(i == j ? -1.0 : 0.0, 0.0);
+    for (int k = 0; k < N; k++) acc = cfma_cj(V[(long long)k * N + i], V[(long long)k * N + j], acc);
+    if (!(fabs(acc.x) <= tol && fabs(acc.y) <= tol)) atomicOr(bad, 1);
+  }
+  if (G_in != nullptr) {
+    for (long long e = t0; e < S * nvar; e += str) {
+      const long long s = e / nvar;
+      const int2 g = tab[e % nvar];
+      const double2 *u = reinterpret_cast<const double2 *>(G_in + s * var_doubles + g.x);
+      const int d = g.y < 0 ? -g.y : g.y;
+      bool okg = true;
+      if (g.y < 0 && !(fabs(u[0].x - 1.0) <= tol && fabs(u[0].y) <= tol && fabs(u[1].x) <= tol &&
+                       fabs(u[1].y) <= tol && fabs(u[2].x) <= tol && fabs(u[2].y) <= tol))
+        okg = false;
+      for (int i = 0; i < d; i++)
+        for (int j = 0; j < d; j++) {
+          double2 acc = make_double2(i == j ? -1.0 : 0.0, 0.0);
+          for (int k = 0; k < d; k++) acc = cfma_cj(u[k * d + i], u[k * d + j], acc);
+          if (!(fabs(acc.x) <= tol && fabs(acc.y) <= tol)) okg = false;
+        }
+      if (!okg) atomicOr(bad, 2);
+    }
+    for (long long e = t0; e < S * var_doubles; e += str) G[e] = G_in[e];
+  }
+  for (long long s = t0; s < S; s += str) {
+    active[s] = (int)s;
+    rec_slot[s] = -1;
+  }
+  if (t0 == 0) {
+    *n_active = (int)S;
+    *counter = 0;
+  }
+}
+
+// a8 in one launch: the per-start summaries and the best start (k_select_best's
+// order: ties -> lowest index, NaN never wins)
+__global__ void __launch_bounds__(1024) k_finish(const double *delta, const int *iters,
+                                                 const int *verdict, int S, qf_summary *out,
+                                                 long long *best) {
+  __shared__ double sd[1024];
+  __shared__ long long si[1024];
+  double bd = NAN;
+  long long bi = -1;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    qf_summary q;
+    q.delta = delta[s];
+    q.iters = iters[s];
+    q.verdict = verdict[s];
+    out[s] = q;
+    if (bi < 0 || better(q.delta, s, bd, bi)) {
+      bd = q.delta;
+      bi = s;
     }
   }
   sd[threadIdx.x] = bd;
@@ -1324,23 +1388,23 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     h2d += (long long)(vslots.size() * sizeof(int2));
   }
   QF_CHECK(cudaMemsetAsync(E.bad(), 0, sizeof(int), st));
-  const int g1 = std::max(1, std::min((int)(((long long)N * N + 255) / 256), E.nsm * 8));
-  k_vdag<<<g1, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), E.vdag(), N);
-  k_check_target<<<g1, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), N, 1e-9, E.bad());
-  E.launches += 2;
-  if (!tab.empty() && d_initial != nullptr) {
-    const long long tot = (long long)S * tab.size();
-    const int g2 = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, E.nsm * 16));
-    k_check_gates<<<g2, 256, 0, st>>>(d_initial, S, (int)tab.size(),
-                                      reinterpret_cast<const int2 *>(W + E.L.gtab), c.var_doubles,
-                                      1e-9, E.bad());
+  int *rec_slot = reinterpret_cast<int *>(W + E.L.rec_slot);
+  {
+    // k_stage: V^dagger + target check, initial gates' checks + copy, active
+    // list, record slots, resident counter -- one launch
+    const long long work = std::max<long long>(
+        {(long long)N * N, (long long)S * (long long)std::max<size_t>(1, tab.size()),
+         d_initial ? (long long)S * c.var_doubles : 0, (long long)S});
+    const int gs = (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, E.nsm * 16));
+    const bool gin = c.var_doubles > 0 && d_initial != nullptr;
+    k_stage<<<gs, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), E.vdag(), N, 1e-9,
+                                E.bad(), gin ? d_initial : nullptr, E.gates(), S, (int)tab.size(),
+                                reinterpret_cast<const int2 *>(W + E.L.gtab), c.var_doubles,
+                                E.active(), E.n_active(), rec_slot, E.n_active() + 2);
     E.launches++;
   }
   QF_CHECK(cudaGetLastError());
-  if (c.var_doubles > 0 && d_initial != nullptr) {
-    QF_CHECK(cudaMemcpyAsync(E.gates(), d_initial, (size_t)S * c.var_doubles * 8,
-                             cudaMemcpyDeviceToDevice, st));
-  } else if (c.var_doubles > 0) {  // seeded starts (initial == NULL), generated in place
+  if (c.var_doubles > 0 && d_initial == nullptr) {  // seeded starts (initial == NULL), generated in place
     std::vector<int4> keys;
     for (int k = 0; k < c.p; k++)
       if (c.kind[k] != QF_GATE_CONSTANT)
@@ -1356,10 +1420,6 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     E.launches++;
     QF_CHECK(cudaGetLastError());
   }
-  int *rec_slot = reinterpret_cast<int *>(W + E.L.rec_slot);
-  k_iota<<<std::max(1, std::min((S + 255) / 256, E.nsm * 4)), 256, 0, st>>>(E.active(), E.n_active(),
-                                                                             S, rec_slot);
-  E.launches++;
   if (p.record_count > 0 && p.record_sweeps > 0) {
     QF_CHECK(cudaMemcpyAsync(W + E.L.rec_starts, p.record_starts, (size_t)p.record_count * 4,
                              cudaMemcpyHostToDevice, st));
@@ -1460,8 +1520,7 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
                                cudaMemcpyHostToDevice, st));
       h2d += (long long)(wdt.size() * sizeof(WDesc));
     }
-    int *counter = E.n_active() + 2;
-    QF_CHECK(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    int *counter = E.n_active() + 2;  // zeroed by k_stage
     ResidentArgs A{};
     A.n = c.n;
     A.N = N;
@@ -1718,12 +1777,11 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
   // ---- a8: summaries and best start
   qf_summary *summ = out.d_summary_out ? out.d_summary_out
                                        : reinterpret_cast<qf_summary *>(W + E.L.summary);
-  k_summaries<<<std::max(1, std::min((S + 255) / 256, E.nsm * 4)), 256, 0, st>>>(
-      reinterpret_cast<double *>(W + E.L.delta), reinterpret_cast<int *>(W + E.L.iters),
-      reinterpret_cast<int *>(W + E.L.verdict), S, summ);
   long long *d_best = reinterpret_cast<long long *>(W + E.L.best);
-  k_select_best<<<1, 1024, 0, st>>>(summ, S, d_best);
-  E.launches += 2;
+  k_finish<<<1, 1024, 0, st>>>(reinterpret_cast<double *>(W + E.L.delta),
+                               reinterpret_cast<int *>(W + E.L.iters),
+                               reinterpret_cast<int *>(W + E.L.verdict), S, summ, d_best);
+  E.launches++;
   QF_CHECK(cudaGetLastError());
   if (out.d_gates_out && c.var_doubles > 0)
     QF_CHECK(cudaMemcpyAsync(out.d_gates_out, E.gates(), (size_t)S * c.var_doubles * 8,
