@@ -216,7 +216,9 @@ def roofline(st, step_ms, w):
         peak, src = fp64_peak_tflops()
         ach = flops / 1e12 / (t_ms / 1e3) if t_ms > 0 else None
         traffic, _ = load_traffic(w.name + ":resident")
-        return {"kernel": "k_resident", "bound": "alu", "achieved": ach, "peak": peak,
+        kname = {0: "k_resident", 1: "k_resident (WIDE)", 2: "k_lean", 3: "k_reg"}.get(
+            st[-1].get("resident_kernel", 0), "k_resident")
+        return {"kernel": kname, "bound": "alu", "achieved": ach, "peak": peak,
                 "unit": "TFLOP/s", "frac": ach / peak if ach else None, "traffic": traffic,
                 "alg_flops_per_launch": flops / len(st), "launches": len(st),
                 "avg_launch_us": 1e3 * t_ms / len(st), "share_of_step": t_ms / step_ms,
