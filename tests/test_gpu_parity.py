@@ -302,17 +302,38 @@ def test_self_target_fixed_point_gpu():
     assert np.abs(r.gates - g0).max() < 1e-12
 
 
-def test_rejects_non_unitary_inputs():
-    w = qfgen.workload("C1")
+@pytest.mark.parametrize("name,engine", [("C1", qf.QF_ENGINE_AUTO), ("C2+", qf.QF_ENGINE_AUTO),
+                                         ("C3", qf.QF_ENGINE_AUTO), ("C1", qf.QF_ENGINE_STREAM)])
+def test_rejects_non_unitary_inputs(name, engine):
+    """Every engine rejects a non-unitary target or initial gate; the resident
+    kernels (k_reg, k_lean, k_resident) check on the device and the call
+    reports the flag with its results, through both APIs."""
+    w = qfgen.workload(name)
     c = qf.Circuit.from_workload(w)
+    init = w.initial(0, 8)
     with pytest.raises(qf.QfError) as e:
-        qf.qf_instantiate(c, 1.01 * w.target_unitary(), w.initial())
+        qf.qf_instantiate(c, 1.01 * w.target_unitary(), init, engine=engine)
     assert e.value.status == qf.QF_E_NOT_UNITARY
-    bad = w.initial()
+    bad = init.copy()
     bad[2, 5] += 1e-3
     with pytest.raises(qf.QfError) as e:
-        qf.qf_instantiate(c, w.target_unitary(), bad)
+        qf.qf_instantiate(c, w.target_unitary(), bad, engine=engine)
     assert e.value.status == qf.QF_E_NOT_UNITARY
+    # the device API without a host result (its own synchronisation point)
+    import torch
+    dev = torch.device("cuda:0")
+    dV = torch.from_numpy(np.ascontiguousarray(1.01 * w.target_unitary())).to(dev)
+    dI = torch.from_numpy(init).to(dev)
+    ws = torch.empty(qf.qf_workspace_size(c, init.shape[0], max_iters=w.max_iters),
+                     dtype=torch.uint8, device=dev)
+    with pytest.raises(qf.QfError) as e:
+        qf.qf_instantiate_device(c, dV, dI, ws, max_iters=w.max_iters, engine=engine,
+                                 want_result=False)
+    assert e.value.status == qf.QF_E_NOT_UNITARY
+    # a good call on the same workspace afterwards is unaffected
+    dV.copy_(torch.from_numpy(np.ascontiguousarray(w.target_unitary())))
+    r = qf.qf_instantiate_device(c, dV, dI, ws, max_iters=3, engine=engine)
+    assert np.all(r.iters <= 3)
 
 
 # ------------------------------------------------------------------ invariance
