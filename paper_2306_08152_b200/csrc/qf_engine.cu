@@ -338,7 +338,8 @@ __global__ void __launch_bounds__(1024) k_select_best(const qf_summary *q, long 
 // workspace, the active list / record slots, and the resident start counter
 __global__ void k_stage(const double2 *V, double2 *Vd, int N, double tol, int *bad,
                         const double *G_in, double *G, long long S, int nvar, const int2 *tab,
-                        int var_doubles, int *active, int *n_active, int *rec_slot, int *counter) {
+                        int var_doubles, int *active, int *n_active, int *rec_slot, int *counter,
+                        int *zero_s) {
   const long long NN = (long long)N * N, str = (long long)gridDim.x * blockDim.x;
   const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (long long e = t0; e < NN; e += str) {
@@ -372,10 +373,12 @@ __global__ void k_stage(const double2 *V, double2 *Vd, int N, double tol, int *b
   for (long long s = t0; s < S; s += str) {
     active[s] = (int)s;
     rec_slot[s] = -1;
+    zero_s[s] = 0;
   }
   if (t0 == 0) {
     *n_active = (int)S;
-    *counter = 0;
+    counter[0] = 0;
+    counter[10] = 0;  // resident time slicing: starts with a verdict (counters word 12)
   }
 }
 
@@ -1400,7 +1403,8 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     k_stage<<<gs, 256, 0, st>>>(reinterpret_cast<const double2 *>(d_target), E.vdag(), N, 1e-9,
                                 E.bad(), gin ? d_initial : nullptr, E.gates(), S, (int)tab.size(),
                                 reinterpret_cast<const int2 *>(W + E.L.gtab), c.var_doubles,
-                                E.active(), E.n_active(), rec_slot, E.n_active() + 2);
+                                E.active(), E.n_active(), rec_slot, E.n_active() + 2,
+                                reinterpret_cast<int *>(W + E.L.plat));
     E.launches++;
   }
   QF_CHECK(cudaGetLastError());
@@ -1544,6 +1548,18 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     // the serial warp gathers its own environment at n <= 4 (C2: 1357 -> 1266 ms
     // to verdict; neutral at C3, C4)
     A.gather_warp = getenv("QF_GATHER_WARP") ? atoi(getenv("QF_GATHER_WARP")) : (c.n <= 4 ? 1 : 0);
+    {
+      // time slicing of the per-start path (section 9: the last partial wave
+      // of starts): slices of reset_iters sweeps; QF_SLICE=0 disables
+      const bool on = !(getenv("QF_SLICE") && atoi(getenv("QF_SLICE")) == 0);
+      const long long nsl = p.reset_iters > 0 ? (p.max_iters + p.reset_iters - 1) / p.reset_iters : 0;
+      if (on && !resident_batch && p.reset_iters > 0 && p.reset_iters < p.max_iters &&
+          nsl * (long long)S < (1LL << 31)) {
+        A.slice = p.reset_iters;
+        A.slice_done = reinterpret_cast<int *>(W + E.L.plat);
+        A.n_done = counter + 10;  // counters word 12 (see k_stage)
+      }
+    }
     A.gather_ltpo_max = getenv("QF_GATHER_LTPO") ? std::max(0, std::min(5, atoi(getenv("QF_GATHER_LTPO")))) : 5;
     A.dist_tol = p.dist_tol;
     A.diff_tol_a = p.diff_tol_a;

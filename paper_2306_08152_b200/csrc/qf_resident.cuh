@@ -93,6 +93,13 @@ struct ResidentArgs {
   // capacity of that region (0: off), ncm = complex entries of cmats
   int gcache, ncm;
   int gather_warp;    // 1: the serial warp gathers the environment itself (no barrier)
+  // time slicing (per-start policy, single problem): a start runs in slices of
+  // `slice` sweeps (= reset_iters, so a slice begins with InitCircuitTensor
+  // exactly where the reset would); tickets t -> (slice t / S, start t % S);
+  // slice_done[s] = next slice of start s, -1 once it has its verdict
+  int slice;
+  int *slice_done;
+  int *n_done;        // starts with a verdict
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
   // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
@@ -910,7 +917,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
   WDesc *wd = reinterpret_cast<WDesc *>(Tm + 256);        // WIDE: transition in W space
   double2 *gcache = reinterpret_cast<double2 *>(tabs + 256);  // SMALL: gates + CONSTANT matrices
   const GateDesc *gdesc = A.gd;  // kernel parameters (constant bank); MULTI: per problem
-  __shared__ int s_start, s_verdict;
+  __shared__ int s_start, s_verdict, s_slice;
   const int tid = threadIdx.x, nt = blockDim.x;
   // the serial work (environment, polar factor, cost) runs on warp sw0 (warp 0;
   // the last warp measured the same)
@@ -920,7 +927,33 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
   __shared__ int s_plat, s_fail, s_bstop;
   unsigned gen = 0;
   for (int pass = 0;; pass++) {
-    if (tid == 0) s_start = A.batch ? (pass == 0 ? (int)blockIdx.x : A.S) : atomicAdd(A.counter, 1);
+    if (tid == 0) {
+      s_slice = 0;
+      if (A.batch) {
+        s_start = pass == 0 ? (int)blockIdx.x : A.S;
+      } else if (A.slice > 0) {
+        // the next ticket whose start still runs; wait for its previous slice
+        const long long nslices = (A.max_iters + A.slice - 1) / A.slice;
+        int st = A.S;
+        for (;;) {
+          if (*(volatile int *)A.n_done >= A.S) break;
+          const long long t = atomicAdd(A.counter, 1);
+          if (t >= nslices * A.S) break;
+          const int r = (int)(t / A.S), sc = (int)(t - (long long)r * A.S);
+          int sd;
+          while ((sd = *(volatile int *)(A.slice_done + sc)) >= 0 && sd < r) __nanosleep(256);
+          if (sd == r) {
+            __threadfence();  // acquire: the previous slice's gates and history
+            st = sc;
+            s_slice = r;
+            break;
+          }
+        }
+        s_start = st;
+      } else {
+        s_start = atomicAdd(A.counter, 1);
+      }
+    }
     if (tid == 0) s_plat = s_fail = s_bstop = 0;
     __syncthreads();
     const int s = s_start;
@@ -977,7 +1010,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       if (s == A.poison && tid == 0) ct[0] = make_double2(NAN, NAN);
       __syncthreads();
     }
-    int it = 0;
+    int it = s_slice * A.slice;  // sweeps already run (time slicing)
     // operands of step j2 into buffer (j2 & 1): all threads gather the
     // environment (VARIABLE gates), the serial warp stages u_old (prefetched
     // into registers during the previous sandwich when `pre`), then the serial
@@ -1275,6 +1308,7 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       } else if (s_verdict != 0) {
         break;
       }
+      if (A.slice > 0 && it % A.slice == 0) break;  // end of this slice (the reset point)
       if (s_fail) continue;  // a failed start (batch policy): nothing to prepare
       if (it % A.reset_iters == 0) res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
       prepare(0, false);  // operands of the next sweep's first step
@@ -1291,6 +1325,15 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       if (V.u0 != u_global) {
         for (int e = tid; e < gcount; e += nt) u_global[e] = V.u0[e];
         __syncthreads();
+      }
+    }
+    if (A.slice > 0 && tid == 0) {  // release the start to its next slice, or retire it
+      __threadfence();
+      if (s_verdict != 0) {
+        *(volatile int *)(A.slice_done + s) = -1;
+        atomicAdd(A.n_done, 1);
+      } else {
+        *(volatile int *)(A.slice_done + s) = it / A.slice;
       }
     }
   }
