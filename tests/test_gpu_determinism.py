@@ -24,6 +24,7 @@ CASES = [
     ("resident SMALL n=3", "C2+", 16, 20, qf.QF_ENGINE_AUTO, {"QF_LEAN": "0"}, {}),
     ("resident SMALL n=4", "C3", 64, 10, qf.QF_ENGINE_AUTO, {}, {}),
     ("resident 128-thread n=6", "C4", 96, 6, qf.QF_ENGINE_AUTO, {}, {}),
+    ("resident time-sliced n=6", "C4", 96, 50, qf.QF_ENGINE_AUTO, {}, {"reset_iters": 20}),
     ("resident WIDE n=6", "C4", 96, 6, qf.QF_ENGINE_AUTO, {"QF_RES_WIDE": "1"}, {}),
     ("resident batch policy", "C3+", 48, 20, qf.QF_ENGINE_AUTO, {},
      {"batch_policy": qf.QF_BATCH_PAPER}),

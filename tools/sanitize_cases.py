@@ -49,6 +49,8 @@ CASES = {
     "res_C2p_small": lambda: run("C2+", 8, 10, env={"QF_LEAN": "0"}),
     "res_C3": lambda: run("C3", 16, 3),
     "res_C4": lambda: run("C4", 6, 2),
+    "res_C4_sliced": lambda: run("C4", 24, 50, reset_iters=20),  # time slicing, waits
+    "res_C3_sliced": lambda: run("C3", 40, 30, reset_iters=10),
     "res_C4_wide": lambda: run("C4", 6, 2, env={"QF_RES_WIDE": "1"}),
     "batch_C3p": lambda: run("C3+", 12, 8, batch_policy=qf.QF_BATCH_PAPER),
     "stream_C4": lambda: run("C4", 6, 1, engine=qf.QF_ENGINE_STREAM),
