@@ -1609,9 +1609,13 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
       const bool rg = reg_ok(c);
       const size_t lsm = ((size_t)(rg ? kRegFixed : kLeanFixed) + A.gstride + A.ncm) * 16;
       const bool bt = p.beta != 0.0;
-      auto lk = rg ? (c.n == 1 ? (bt ? k_reg<1, true> : k_reg<1, false>)
-                      : c.n == 2 ? (bt ? k_reg<2, true> : k_reg<2, false>)
-                                 : (bt ? k_reg<3, true> : k_reg<3, false>))
+      bool v4 = false;  // 2-qubit VARIABLE gates present
+      for (int k = 0; k < c.p; k++) v4 |= c.kind[k] == QF_GATE_VARIABLE && c.arity[k] == 2;
+      auto lk = rg ? (c.n == 1 ? (bt ? k_reg<1, true, false> : k_reg<1, false, false>)
+                      : c.n == 2 ? (v4 ? (bt ? k_reg<2, true, true> : k_reg<2, false, true>)
+                                       : (bt ? k_reg<2, true, false> : k_reg<2, false, false>))
+                                 : (v4 ? (bt ? k_reg<3, true, true> : k_reg<3, false, true>)
+                                       : (bt ? k_reg<3, true, false> : k_reg<3, false, false>)))
                    : (c.n == 1 ? k_lean<1> : c.n == 2 ? k_lean<2> : k_lean<3>);
       QF_CHECK(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
       int lper = 0;

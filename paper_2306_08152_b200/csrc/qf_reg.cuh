@@ -54,7 +54,9 @@ __device__ __forceinline__ double2 reg_fetch_u(const double2 (&v)[RegShape<NQ>::
 
 constexpr int kRegFixed = 6 * 16;  // L, R, u_old, P, A, V of a 4 x 4 VARIABLE update
 
-template <int NQ, bool BETA>
+// VAR4: the template has 2-qubit VARIABLE gates (their update code costs the
+// one-qubit-only templates ~10 % per step in registers and scheduling)
+template <int NQ, bool BETA, bool VAR4 = true>
 __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs A) {
   if (A.bad != nullptr && *A.bad != 0) return;  // rejected input (host reports it)
   using RS = RegShape<NQ>;
@@ -268,8 +270,8 @@ __global__ void __launch_bounds__(32) k_reg(const __grid_constant__ ResidentArgs
       } else {  // 4 x 4: left pass, then right pass (k_lean pass4)
         const double2 *M = cm + g.goff;
         const int a1 = g.abits[1], a2 = g.abits[2];
-        const bool var4 = g.kind != 1;
-        if (var4) {
+        const bool var4 = VAR4 && g.kind != 1;
+        if constexpr (VAR4) if (var4) {
           // VARIABLE (as k_lean's prepare): P = PT(ct) on lanes 0..15 (rests
           // ascending), A = E^dagger, warp_polar, then L / R in shared memory
           const int p0 = __ffs(mask) - 1, p1 = 31 - __clz(mask);
