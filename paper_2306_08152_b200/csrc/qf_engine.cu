@@ -1550,14 +1550,17 @@ qf_status engine_run(const qf_circuit_s &c, const double *d_target, const double
     A.gather_warp = getenv("QF_GATHER_WARP") ? atoi(getenv("QF_GATHER_WARP")) : (c.n <= 4 ? 1 : 0);
     {
       // time slicing of the per-start path (section 9: the last partial wave
-      // of starts): slices of reset_iters sweeps; QF_SLICE=0 disables
-      const bool on = !(getenv("QF_SLICE") && atoi(getenv("QF_SLICE")) == 0);
-      const long long nsl = p.reset_iters > 0 ? (p.max_iters + p.reset_iters - 1) / p.reset_iters : 0;
-      if (on && !resident_batch && p.reset_iters > 0 && p.reset_iters < p.max_iters &&
+      // of starts): slices of min(reset_iters, 10) sweeps (QF_SLICE=k sets k,
+      // QF_SLICE=0 disables)
+      int sl = p.reset_iters > 0 ? std::min(p.reset_iters, 10) : 10;
+      if (const char *e = getenv("QF_SLICE")) sl = atoi(e);
+      const long long nsl = sl > 0 ? (p.max_iters + sl - 1) / sl : 0;
+      if (sl > 0 && !resident_batch && p.reset_iters > 0 && sl < p.max_iters &&
           nsl * (long long)S < (1LL << 31)) {
-        A.slice = p.reset_iters;
+        A.slice = sl;
         A.slice_done = reinterpret_cast<int *>(W + E.L.plat);
         A.n_done = counter + 10;  // counters word 12 (see k_stage)
+        A.ct_store = E.ct();      // the streaming engine's tensors, unused here
       }
     }
     A.gather_ltpo_max = getenv("QF_GATHER_LTPO") ? std::max(0, std::min(5, atoi(getenv("QF_GATHER_LTPO")))) : 5;

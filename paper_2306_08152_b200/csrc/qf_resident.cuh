@@ -94,12 +94,14 @@ struct ResidentArgs {
   int gcache, ncm;
   int gather_warp;    // 1: the serial warp gathers the environment itself (no barrier)
   // time slicing (per-start policy, single problem): a start runs in slices of
-  // `slice` sweeps (= reset_iters, so a slice begins with InitCircuitTensor
-  // exactly where the reset would); tickets t -> (slice t / S, start t % S);
+  // `slice` sweeps; a slice that begins on a reset point begins with
+  // InitCircuitTensor exactly where the reset would, any other one restores the
+  // tensor its predecessor saved (ct_store); tickets t -> (slice t / S, start t % S);
   // slice_done[s] = next slice of start s, -1 once it has its verdict
   int slice;
   int *slice_done;
   int *n_done;        // starts with a verdict
+  double2 *ct_store;  // slice ends off the reset points: the tensor, N^2 per start
   int gather_ltpo_max;  // log2 of the most threads per environment output (<= 5)
   // batch policy (NEXT-1) with the whole batch co-resident: one CTA per start
   // (blockIdx.x), a grid barrier after every sweep, per-sweep counts
@@ -1005,10 +1007,17 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       fw = j >= V.p;
       return fw ? j - V.p : V.p - 1 - j;
     };
-    res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
-    if (A.poison >= 0) {  // fault injection for the NUMERIC_FAIL tests (QF_DEBUG_POISON)
-      if (s == A.poison && tid == 0) ct[0] = make_double2(NAN, NAN);
+    if (A.slice > 0 && (s_slice * A.slice) % A.reset_iters != 0) {
+      // a slice off the reset points: the tensor its predecessor left
+      const double2 *src = A.ct_store + (long long)s * V.N * V.N;
+      for (int e = tid; e < V.N * V.N; e += nt) ct[e] = src[e];
       __syncthreads();
+    } else {
+      res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
+      if (A.poison >= 0) {  // fault injection for the NUMERIC_FAIL tests (QF_DEBUG_POISON)
+        if (s == A.poison && tid == 0) ct[0] = make_double2(NAN, NAN);
+        __syncthreads();
+      }
     }
     int it = s_slice * A.slice;  // sweeps already run (time slicing)
     // operands of step j2 into buffer (j2 & 1): all threads gather the
@@ -1308,7 +1317,13 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
       } else if (s_verdict != 0) {
         break;
       }
-      if (A.slice > 0 && it % A.slice == 0) break;  // end of this slice (the reset point)
+      if (A.slice > 0 && it % A.slice == 0) {  // end of this slice
+        if (it % A.reset_iters != 0) {  // off a reset point: keep the tensor
+          double2 *dst = A.ct_store + (long long)s * V.N * V.N;
+          for (int e = tid; e < V.N * V.N; e += nt) dst[e] = ct[e];
+        }
+        break;
+      }
       if (s_fail) continue;  // a failed start (batch policy): nothing to prepare
       if (it % A.reset_iters == 0) res_init<MAXD, WIDE>(A, V, ct, gdesc, s, Lb);
       prepare(0, false);  // operands of the next sweep's first step
@@ -1326,6 +1341,10 @@ __global__ void __launch_bounds__(WIDE ? 256 : (SMALL ? 64 : 128), SMALL ? 8 : 3
         for (int e = tid; e < gcount; e += nt) u_global[e] = V.u0[e];
         __syncthreads();
       }
+    }
+    if (A.slice > 0) {  // every thread's tensor / gate writes before the release
+      __threadfence();
+      __syncthreads();
     }
     if (A.slice > 0 && tid == 0) {  // release the start to its next slice, or retire it
       __threadfence();

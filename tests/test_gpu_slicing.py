@@ -1,8 +1,9 @@
 """Time slicing of the resident engine (per-start policy): a start runs in
-slices of reset_iters sweeps, each slice beginning with InitCircuitTensor
-exactly where the reset (reading R10) would rebuild the tensor, so every
-per-start result is bitwise the one of a start run to its verdict in one CTA
-(QF_SLICE=0).  Cases: more starts than resident CTAs and fewer (a start's next
+slices of min(reset_iters, 10) sweeps; a slice beginning on a reset point
+begins with InitCircuitTensor exactly where the reset (reading R10) would
+rebuild the tensor, any other one restores the tensor its predecessor saved,
+so every per-start result is bitwise the one of a start run to its verdict in
+one CTA (QF_SLICE=0).  Cases: more starts than resident CTAs and fewer (a start's next
 slice then waits on its previous one), the SMALL (n <= 4) and 128-thread
 (n = 6) kernels, records across slice boundaries, a start that fails."""
 import numpy as np
@@ -29,6 +30,7 @@ def _run(w, S, monkeypatch, slice_on, **kw):
     ("C4", 700, 60, 20),     # more starts than CTAs
     ("C3", 200, 90, 30),     # SMALL kernel
     ("C3+", 64, 50, 7),      # short slices, starts converging inside a slice
+    ("C4", 300, 60, 13),     # slices of 10 across resets at 13, 26, ...: saved tensors
 ])
 def test_slicing_bitwise(name, S, iters, reset, monkeypatch):
     w = qfgen.workload(name)
